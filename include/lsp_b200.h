@@ -1,0 +1,241 @@
+/*
+ * lsp_b200.h -- C-ABI of the B200-native LSP (d,r)-sparse projector path.
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * (lspkit `lsp_core`, /root/reference/proj).  Each entry point names the
+ * reference interface it replaces (file:line under /root/reference).  Plain C
+ * types only: host pointers where the reference takes lsp::Matrix /
+ * lsp::SparseProjector by value, device pointers (and a caller-owned
+ * cudaStream_t passed as void*) for the device-resident hot path.
+ *
+ * Naming follows the reference: `d` is the subspace width and `r` the number
+ * of nonzeros per projector row (BASELINE.json calls them r and d).
+ *
+ * Conventions
+ *  - Status: every function returns lsp_status; LSP_OK == 0.  The reference's
+ *    exception taxonomy maps as  std::invalid_argument -> LSP_EINVAL,
+ *    lsp::NumericError -> LSP_ENUMERIC, lsp::IoError -> LSP_EIO
+ *    (proj/include/lsp/common.hpp:13-31).  lsp_last_error() returns the
+ *    message of the last failure on the calling host thread.
+ *  - Ownership: device buffers passed in are caller-owned; handles are
+ *    library-owned and released with the matching *_destroy.  A pair keeps
+ *    pointers to its two projectors (they must outlive it).
+ *  - Asynchrony: functions taking a stream enqueue work on it and return
+ *    without synchronising, unless documented as synchronous.
+ *  - Threading: handles may be used from any host thread, but not
+ *    concurrently on the same handle (one handle per layer).
+ *  - Layout: dense matrices are row-major with an explicit leading dimension
+ *    in ELEMENTS.  s x s subspace matrices (S, delta, Adam moments) may be
+ *    passed in the reference layout (LSP_LAYOUT_ROW: X[a][b] at a*d+b) or
+ *    transposed (LSP_LAYOUT_T: X[a][b] at b*d+a), the layout the fused device
+ *    path uses internally.
+ */
+#ifndef LSP_B200_H_
+#define LSP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSP_B200_VERSION 1
+
+typedef enum {
+  LSP_OK = 0,
+  LSP_EINVAL = 1,   /* std::invalid_argument */
+  LSP_ENUMERIC = 2, /* lsp::NumericError */
+  LSP_EIO = 3,      /* lsp::IoError */
+  LSP_ECUDA = 4,    /* CUDA runtime failure (incl. no device) */
+  LSP_ENOMEM = 5
+} lsp_status;
+
+typedef enum { LSP_F64 = 0, LSP_F32 = 1, LSP_BF16 = 2 } lsp_dtype;
+typedef enum { LSP_LAYOUT_ROW = 0, LSP_LAYOUT_T = 1 } lsp_layout;
+/* proj/include/lsp/projector.hpp:38-41 */
+typedef enum { LSP_REG_SQUARED = 0, LSP_REG_UNSQUARED = 1 } lsp_reg_kind;
+/* proj/include/lsp/subspace_opt.hpp:39-42 */
+typedef enum { LSP_TRANSFER_ENTRYWISE = 0, LSP_TRANSFER_MATRIX = 1 } lsp_transfer_kind;
+
+typedef struct lsp_projector_s* lsp_projector_t; /* device SparseProjector (CSR + CSC) */
+typedef struct lsp_pair_s* lsp_pair_t;           /* ProjectorPair + device workspace   */
+typedef struct lsp_adam_s* lsp_adam_t;           /* device SubspaceOptState            */
+typedef void* lsp_stream_t;                      /* cudaStream_t (NULL = legacy stream) */
+
+/* proj/include/lsp/projector.hpp:43-51 */
+typedef struct {
+  double alpha;
+  double reg_beta;
+  double step_size;
+  int max_steps;
+  int timeout_steps;
+  uint64_t seed;
+  int reg_kind; /* lsp_reg_kind */
+} lsp_fit_config;
+
+/* proj/include/lsp/projector.hpp:53-60 (loss_curve returned separately) */
+typedef struct {
+  double final_rel_bias;
+  int success;
+  int timed_out;
+  int stalled;
+  int steps;
+  int n_loss; /* total entries of the loss curve (may exceed max_curve) */
+} lsp_fit_report;
+
+/* ----------------------------------------------------------------------------
+ * Library / device
+ * -------------------------------------------------------------------------- */
+const char* lsp_last_error(void);
+int lsp_version(void);
+/* Synchronous: number of usable CUDA devices (0 without a GPU). */
+int lsp_device_count(int* count);
+/* Number of kernels this library has launched in this process (all handles);
+ * used by bench.py to report gpu_launches. */
+uint64_t lsp_launch_count(void);
+/* Default values of lsp_fit_config (projector.hpp:43-51). */
+lsp_fit_config lsp_fit_config_default(void);
+
+/* ----------------------------------------------------------------------------
+ * Host-side projector construction and text I/O (no GPU needed)
+ * -------------------------------------------------------------------------- */
+/* proj/include/lsp/common.hpp:42-45 */
+uint64_t lsp_derive_seed(uint64_t master, uint64_t tag, uint64_t index);
+/* proj/src/projector.cpp:66-85 -- bit-exact positions and values (mt19937_64,
+ * partial Fisher-Yates, Box-Muller).  pos/val hold n_rows*r entries. */
+int lsp_init_sparse(int n_rows, int d, int r, uint64_t seed, int32_t* pos, double* val);
+/* proj/src/projector.cpp:87-96 (d = n_rows, r = 1, value 1) */
+int lsp_identity_pattern(int n_rows, int32_t* pos, double* val);
+/* proj/src/projector.cpp:317-327.  Writes up to cap bytes (NUL-terminated) and
+ * returns, via *needed, the full size including the NUL. */
+int lsp_save_projector(int n_rows, int d, int r, const int32_t* pos, const double* val,
+                       char* buf, int64_t cap, int64_t* needed);
+/* proj/src/projector.cpp:329-354.  Two calls: with pos == NULL only the header
+ * is parsed into *n_rows, *d, *r; then again with arrays of n_rows*r entries.
+ * Malformed input -> LSP_EIO with the reference's messages. */
+int lsp_load_projector(const char* text, int64_t len, int* n_rows, int* d, int* r,
+                       int32_t* pos, double* val);
+/* proj/src/trainer.cpp:60-72 */
+int lsp_subsample_size(double gamma_bound, double chernoff_beta, int m, int n,
+                       int total_steps, double delta, int64_t* out);
+
+/* ----------------------------------------------------------------------------
+ * Device projectors and pairs
+ * -------------------------------------------------------------------------- */
+/* Uploads a SparseProjector (proj/include/lsp/projector.hpp:18-30): validates
+ * it like load_projector (positions in [0,d), strictly ascending per row,
+ * finite values) and builds the CSR and CSC device arrays.  compute = LSP_F32
+ * or LSP_F64 selects the value/accumulator precision of every kernel that
+ * uses this projector. Synchronous. */
+int lsp_projector_create(int n_rows, int d, int r, const int32_t* pos, const double* val,
+                         lsp_dtype compute, lsp_projector_t* out);
+/* Replace the values (positions are frozen, as in fit). Synchronous. */
+int lsp_projector_set_values(lsp_projector_t p, const double* val);
+/* Download positions and values (either may be NULL). Synchronous. */
+int lsp_projector_get(lsp_projector_t p, int32_t* pos, double* val);
+int lsp_projector_shape(lsp_projector_t p, int* n_rows, int* d, int* r);
+int lsp_projector_destroy(lsp_projector_t p);
+
+/* ProjectorPair (projector.hpp:32-36); P has m rows, Q has n rows.
+ * P.d != Q.d -> LSP_EINVAL ("projector pair: P.d != Q.d", projector.cpp:20-23). */
+int lsp_pair_create(lsp_projector_t p, lsp_projector_t q, lsp_pair_t* out);
+int lsp_pair_destroy(lsp_pair_t pair);
+
+/* ----------------------------------------------------------------------------
+ * Hot path (device pointers, asynchronous on `stream`)
+ * -------------------------------------------------------------------------- */
+/* compress: S = P^T G Q  (projector.cpp:163-168).  g is m x n (ldg elements)
+ * of g_dtype; s is d x d in the pair's compute dtype and the given layout. */
+int lsp_compress(lsp_pair_t pair, const void* g, int64_t ldg, lsp_dtype g_dtype, void* s,
+                 lsp_layout s_layout, lsp_stream_t stream);
+/* decompress: out = P S Q^T  (projector.cpp:170-175); out is m x n of out_dtype. */
+int lsp_decompress(lsp_pair_t pair, const void* s, lsp_layout s_layout, void* out,
+                   int64_t ldo, lsp_dtype out_dtype, lsp_stream_t stream);
+/* Fused decompress-and-apply: w -= lr * P delta Q^T in one read-modify-write
+ * pass over w (the apply of proj/src/trainer.cpp:190). */
+int lsp_decompress_apply(lsp_pair_t pair, const void* delta, lsp_layout delta_layout,
+                         double lr, void* w, int64_t ldw, lsp_dtype w_dtype,
+                         lsp_stream_t stream);
+/* estimation_bias: out = P P^T sigma Q Q^T - sigma  (projector.cpp:177-181). */
+int lsp_estimation_bias(lsp_pair_t pair, const void* sigma, int64_t lds, lsp_dtype dtype,
+                        void* out, int64_t ldo, lsp_stream_t stream);
+/* relative_bias: |b(sigma)|_F / |sigma|_F (projector.cpp:183-187).
+ * SYNCHRONOUS (returns a host double). Zero sigma -> LSP_EINVAL. */
+int lsp_relative_bias(lsp_pair_t pair, const void* sigma, int64_t lds, lsp_dtype dtype,
+                      double* out, lsp_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Subspace Adam (proj/include/lsp/subspace_opt.hpp:17-37)
+ * -------------------------------------------------------------------------- */
+/* make_opt_state(rows, cols, beta1, beta2, eps) (subspace_opt.cpp:17-33);
+ * moments zero-initialised on the device in the given compute dtype and
+ * stored in `layout` (the fused path, lsp_step/lsp_update, needs LSP_LAYOUT_T). */
+int lsp_adam_create(int rows, int cols, double beta1, double beta2, double eps,
+                    lsp_dtype compute, lsp_layout layout, lsp_adam_t* out);
+int lsp_adam_destroy(lsp_adam_t st);
+/* adam_step (subspace_opt.cpp:35-57): grad (device, rows x cols, compute dtype,
+ * same layout as the stored moments) -> moments updated in place, delta
+ * (bias-corrected M/(sqrt(V)+eps), no learning rate) written to `delta`.
+ * A non-finite gradient leaves M, V and delta untouched and latches a device
+ * flag that lsp_adam_check reports as LSP_ENUMERIC (reference semantics:
+ * NumericError before any state change). */
+int lsp_adam_step(lsp_adam_t st, const void* grad, void* delta, lsp_stream_t stream);
+/* SYNCHRONOUS: LSP_ENUMERIC if a non-finite gradient was seen since the last
+ * check (and clears the flag), else LSP_OK. */
+int lsp_adam_check(lsp_adam_t st, lsp_stream_t stream);
+/* SYNCHRONOUS host copies of the state as doubles in the given layout. */
+int lsp_adam_get(lsp_adam_t st, double* m, double* v, int64_t* step, lsp_layout layout);
+int lsp_adam_set(lsp_adam_t st, const double* m, const double* v, int64_t step,
+                 lsp_layout layout);
+int lsp_adam_info(lsp_adam_t st, int* rows, int* cols, double* beta1, double* beta2,
+                  double* eps);
+
+/* ----------------------------------------------------------------------------
+ * Fused per-matrix step: compress -> Adam -> decompress-and-apply, i.e. one
+ * iteration of the per-layer loop of proj/src/trainer.cpp:187-190, with S,
+ * the moments and delta kept in the transposed device layout.  `s_out` (may
+ * be NULL) receives S^T.  The Adam state must be d x d.
+ * -------------------------------------------------------------------------- */
+int lsp_step(lsp_pair_t pair, lsp_adam_t st, const void* g, int64_t ldg, lsp_dtype g_dtype,
+             void* w, int64_t ldw, lsp_dtype w_dtype, double lr, void* s_out,
+             lsp_stream_t stream);
+/* Data-parallel split of lsp_step: the caller all-reduces the S^T produced by
+ * lsp_compress(..., LSP_LAYOUT_T, ...) (mean over ranks), then calls
+ * lsp_update to run Adam and the decompress-and-apply. */
+int lsp_update(lsp_pair_t pair, lsp_adam_t st, const void* s_t, void* w, int64_t ldw,
+               lsp_dtype w_dtype, double lr, lsp_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Projector fit (proj/src/projector.cpp:189-315), on the device in fp64.
+ * targets: T device pointers to m x n matrices (ld, dtype shared).
+ * -------------------------------------------------------------------------- */
+/* fit_loss (projector.cpp:189-198). SYNCHRONOUS. */
+int lsp_fit_loss(lsp_pair_t pair, const void* const* targets, int t, int64_t ld,
+                 lsp_dtype dtype, const lsp_fit_config* cfg, double* loss, lsp_stream_t stream);
+/* fit_gradient (projector.cpp:200-236): host arrays laid out like values
+ * (m*r and n*r). SYNCHRONOUS. */
+int lsp_fit_gradient(lsp_pair_t pair, const void* const* targets, int t, int64_t ld,
+                     lsp_dtype dtype, const lsp_fit_config* cfg, double* grad_p,
+                     double* grad_q, lsp_stream_t stream);
+/* fit (projector.cpp:253-315): updates the pair's projector values in place.
+ * loss_curve (may be NULL) receives up to max_curve losses. SYNCHRONOUS. */
+int lsp_fit(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_dtype dtype,
+            const lsp_fit_config* cfg, lsp_fit_report* report, double* loss_curve,
+            int max_curve, lsp_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Optimizer-state transfer after a refit (proj/src/subspace_opt.cpp:59-101)
+ * -------------------------------------------------------------------------- */
+/* projector_gram: out = A^T B (A.d x B.d, row-major fp64, device). */
+int lsp_projector_gram(lsp_projector_t a, lsp_projector_t b, double* out,
+                       lsp_stream_t stream);
+/* reproject_state: M <- (Pn^T Po) M (Qo^T Qn), V likewise with entrywise- or
+ * matrix-squared transfer maps, clamped at zero.  In place on `st`. */
+int lsp_reproject_state(lsp_adam_t st, lsp_pair_t old_pair, lsp_pair_t new_pair,
+                        lsp_transfer_kind kind, lsp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSP_B200_H_ */

@@ -1,0 +1,552 @@
+// extern "C" boundary (include/lsp_b200.h): argument validation with the
+// reference's error semantics, handle management, and orchestration of the
+// device kernels.  No compute happens on the host except index generation.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "core.cuh"
+#include "host_projector.h"
+
+struct lsp_projector_s : lspb::Projector {};
+struct lsp_pair_s : lspb::Pair {};
+struct lsp_adam_s : lspb::Adam {};
+
+namespace lspb {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local std::string g_last_error;
+
+size_t dtype_size(lsp_dtype t) {
+  switch (t) {
+    case LSP_F64: return 8;
+    case LSP_F32: return 4;
+    case LSP_BF16: return 2;
+  }
+  fail(LSP_EINVAL, "unknown dtype");
+}
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return v > 0 ? v : 148;
+  }();
+  return sms;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return LSP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = "host allocation failed";
+    return LSP_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LSP_EINVAL;
+  }
+}
+
+// ---- Projector ---------------------------------------------------------------
+static void upload(DevBuf& b, const void* src, size_t bytes) {
+  b.ensure(std::max<size_t>(bytes, 16));
+  if (bytes) LSP_CUDA(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
+}
+
+template <typename T>
+static std::vector<T> cast_values(const std::vector<double>& v) {
+  return std::vector<T>(v.begin(), v.end());
+}
+
+void Projector::upload_values() {
+  LSP_DISPATCH_ACC(compute, T, {
+    auto cv = cast_values<T>(h_val);
+    upload(val, cv.data(), cv.size() * sizeof(T));
+  })
+  launch_refresh_values(*this, nullptr);
+  LSP_CUDA(cudaDeviceSynchronize());
+}
+
+void Projector::refresh_values(cudaStream_t st) { launch_refresh_values(*this, st); }
+
+const ChunkTable& Projector::chunk_table(int bm) {
+  for (auto& c : chunks)
+    if (c->bm == bm) return *c;
+  auto ct = std::make_unique<ChunkTable>();
+  ct->bm = bm;
+  ct->nchunks = ceil_div(n_rows, bm);
+  std::vector<int32_t> split, rows, perm;
+  build_chunks(n_rows, d, bm, h_csc_ptr, h_csc_rows, h_csc_perm, split, rows, perm);
+  upload(ct->split, split.data(), split.size() * sizeof(int32_t));
+  upload(ct->perm, perm.data(), perm.size() * sizeof(int32_t));
+  LSP_DISPATCH_ACC(compute, T, {
+    using E = typename EntryOf<T>::type;
+    std::vector<E> ent(rows.size());
+    for (size_t t = 0; t < rows.size(); ++t) {
+      ent[t] = E{};
+      ent[t].off = rows[t] * 32;
+      ent[t].val = static_cast<T>(h_val[perm[t]]);
+    }
+    upload(ct->ent, ent.data(), ent.size() * sizeof(E));
+  })
+  chunks.push_back(std::move(ct));
+  return *chunks.back();
+}
+
+int* Pair::flag_ptr() {
+  if (!flag.p) {
+    flag.ensure(sizeof(int));
+    LSP_CUDA(cudaMemset(flag.p, 0, sizeof(int)));
+  }
+  return flag.as<int>();
+}
+
+static lsp_projector_s* make_projector(int n_rows, int d, int r, const int32_t* pos,
+                                 const double* val, lsp_dtype compute) {
+  require(compute == LSP_F32 || compute == LSP_F64, "projector compute dtype must be F32 or F64");
+  require(pos && val, "projector: null arrays");
+  validate_projector(n_rows, d, r, pos, val, LSP_EINVAL);
+  auto P = std::make_unique<lsp_projector_s>();
+  P->n_rows = n_rows;
+  P->d = d;
+  P->r = r;
+  P->compute = compute;
+  const size_t nnz = P->nnz();
+  P->h_pos.assign(pos, pos + nnz);
+  P->h_val.assign(val, val + nnz);
+  build_csc(n_rows, d, r, pos, P->h_csc_ptr, P->h_csc_rows, P->h_csc_perm);
+  upload(P->pos, pos, nnz * sizeof(int32_t));
+  upload(P->csc_ptr, P->h_csc_ptr.data(), P->h_csc_ptr.size() * sizeof(int32_t));
+  upload(P->csc_row, P->h_csc_rows.data(), nnz * sizeof(int32_t));
+  upload(P->csc_perm, P->h_csc_perm.data(), nnz * sizeof(int32_t));
+  P->csc_val.ensure(std::max<size_t>(nnz * P->vsize(), 16));
+  P->upload_values();
+  return P.release();
+}
+
+double sumsq_sync(Pair& pr, int rows, int cols, const void* x, long long ld, lsp_dtype dt,
+                  cudaStream_t st) {
+  // gather with zero entries per row and beta = 1: the result is x itself,
+  // whose squares the kernel sums deterministically.
+  int np = 0;
+  launch_gather(rows, cols, nullptr, 0, nullptr, nullptr, pr.compute, x, ld, dt, x, ld, nullptr,
+                0, dt, 0.0, 1.0, &pr.red, &np, st);
+  return reduce_partials_sync(pr.red.as<double>(), np, st);
+}
+
+}  // namespace lspb
+
+using namespace lspb;
+
+template <typename T>
+static void moments_to_host(const Adam& a, const DevBuf& b, double* out, lsp_layout layout) {
+  std::vector<T> tmp(a.count());
+  LSP_CUDA(cudaMemcpy(tmp.data(), b.p, tmp.size() * sizeof(T), cudaMemcpyDeviceToHost));
+  const bool tr = layout != a.layout;
+  // stored layout: ROW -> [r][c] at r*cols+c ; T -> [r][c] at c*rows+r
+  for (int r = 0; r < a.rows; ++r)
+    for (int c = 0; c < a.cols; ++c) {
+      const size_t src = a.layout == LSP_LAYOUT_ROW ? static_cast<size_t>(r) * a.cols + c
+                                                    : static_cast<size_t>(c) * a.rows + r;
+      const size_t dst = (tr ? layout : a.layout) == LSP_LAYOUT_ROW
+                             ? static_cast<size_t>(r) * a.cols + c
+                             : static_cast<size_t>(c) * a.rows + r;
+      out[dst] = static_cast<double>(tmp[src]);
+    }
+}
+
+template <typename T>
+static void moments_from_host(const Adam& a, DevBuf& b, const double* in, lsp_layout layout) {
+  std::vector<T> tmp(a.count());
+  for (int r = 0; r < a.rows; ++r)
+    for (int c = 0; c < a.cols; ++c) {
+      const size_t src = layout == LSP_LAYOUT_ROW ? static_cast<size_t>(r) * a.cols + c
+                                                  : static_cast<size_t>(c) * a.rows + r;
+      const size_t dst = a.layout == LSP_LAYOUT_ROW ? static_cast<size_t>(r) * a.cols + c
+                                                    : static_cast<size_t>(c) * a.rows + r;
+      tmp[dst] = static_cast<T>(in[src]);
+    }
+  LSP_CUDA(cudaMemcpy(b.p, tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+extern "C" {
+
+const char* lsp_last_error(void) { return g_last_error.c_str(); }
+int lsp_version(void) { return LSP_B200_VERSION; }
+uint64_t lsp_launch_count(void) { return g_launches.load(); }
+
+int lsp_device_count(int* count) {
+  return guard([&] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+lsp_fit_config lsp_fit_config_default(void) {
+  lsp_fit_config c;
+  c.alpha = 0.1;
+  c.reg_beta = 0.0;
+  c.step_size = 1e-2;
+  c.max_steps = 500;
+  c.timeout_steps = 500;
+  c.seed = 0;
+  c.reg_kind = LSP_REG_SQUARED;
+  return c;
+}
+
+uint64_t lsp_derive_seed(uint64_t master, uint64_t tag, uint64_t index) {
+  return derive_seed(master, tag, index);
+}
+
+int lsp_init_sparse(int n_rows, int d, int r, uint64_t seed, int32_t* pos, double* val) {
+  return guard([&] { init_sparse(n_rows, d, r, seed, pos, val); });
+}
+
+int lsp_identity_pattern(int n_rows, int32_t* pos, double* val) {
+  return guard([&] {
+    require(n_rows >= 1, "identity_pattern: n_rows must be >= 1");
+    for (int i = 0; i < n_rows; ++i) {
+      pos[i] = i;
+      val[i] = 1.0;
+    }
+  });
+}
+
+int lsp_save_projector(int n_rows, int d, int r, const int32_t* pos, const double* val,
+                       char* buf, int64_t cap, int64_t* needed) {
+  return guard([&] {
+    const std::string s = save_projector_text(n_rows, d, r, pos, val);
+    if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
+    if (buf && cap > 0) {
+      const size_t nc = std::min<size_t>(static_cast<size_t>(cap - 1), s.size());
+      std::memcpy(buf, s.data(), nc);
+      buf[nc] = '\0';
+    }
+  });
+}
+
+int lsp_load_projector(const char* text, int64_t len, int* n_rows, int* d, int* r,
+                       int32_t* pos, double* val) {
+  return guard([&] {
+    require(text != nullptr, "load_projector: null text");
+    const std::string s(text, len >= 0 ? static_cast<size_t>(len) : std::strlen(text));
+    load_projector_text(s, n_rows, d, r, pos, val);
+  });
+}
+
+int lsp_subsample_size(double gamma_bound, double chernoff_beta, int m, int n, int total_steps,
+                       double delta, int64_t* out) {
+  return guard([&] { *out = subsample_size(gamma_bound, chernoff_beta, m, n, total_steps, delta); });
+}
+
+// ---- projectors / pairs --------------------------------------------------------
+int lsp_projector_create(int n_rows, int d, int r, const int32_t* pos, const double* val,
+                         lsp_dtype compute, lsp_projector_t* out) {
+  return guard([&] {
+    *out = make_projector(n_rows, d, r, pos, val, compute);
+  });
+}
+
+int lsp_projector_set_values(lsp_projector_t p, const double* val) {
+  return guard([&] {
+    require(p && val, "projector_set_values: null argument");
+    validate_projector(p->n_rows, p->d, p->r, p->h_pos.data(), val, LSP_EINVAL);
+    p->h_val.assign(val, val + p->nnz());
+    p->upload_values();
+  });
+}
+
+int lsp_projector_get(lsp_projector_t p, int32_t* pos, double* val) {
+  return guard([&] {
+    require(p != nullptr, "projector_get: null handle");
+    if (pos) std::copy(p->h_pos.begin(), p->h_pos.end(), pos);
+    if (val) {
+      LSP_DISPATCH_ACC(p->compute, T, {
+        std::vector<T> tmp(p->nnz());
+        LSP_CUDA(cudaMemcpy(tmp.data(), p->val.p, tmp.size() * sizeof(T), cudaMemcpyDeviceToHost));
+        if (p->compute == LSP_F64)
+          std::copy(tmp.begin(), tmp.end(), val);
+        else  // fp32 device copy: report the exact host values the caller gave
+          std::copy(p->h_val.begin(), p->h_val.end(), val);
+      })
+    }
+  });
+}
+
+int lsp_projector_shape(lsp_projector_t p, int* n_rows, int* d, int* r) {
+  return guard([&] {
+    require(p != nullptr, "projector_shape: null handle");
+    if (n_rows) *n_rows = p->n_rows;
+    if (d) *d = p->d;
+    if (r) *r = p->r;
+  });
+}
+
+int lsp_projector_destroy(lsp_projector_t p) {
+  return guard([&] { delete p; });
+}
+
+int lsp_pair_create(lsp_projector_t p, lsp_projector_t q, lsp_pair_t* out) {
+  return guard([&] {
+    require(p && q && out, "pair_create: null argument");
+    if (p->d != q->d) fail(LSP_EINVAL, "projector pair: P.d != Q.d");
+    require(p->compute == q->compute, "pair_create: P and Q compute dtypes differ");
+    auto* pr = new lsp_pair_s();
+    pr->p = p;
+    pr->q = q;
+    pr->m = p->n_rows;
+    pr->n = q->n_rows;
+    pr->d = p->d;
+    pr->compute = p->compute;
+    *out = pr;
+  });
+}
+
+int lsp_pair_destroy(lsp_pair_t pair) {
+  return guard([&] { delete pair; });
+}
+
+// ---- hot path ------------------------------------------------------------------
+static void check_ld(long long ld, int cols, const char* what) {
+  if (ld < cols) fail(LSP_EINVAL, std::string(what) + ": leading dimension smaller than columns");
+}
+
+int lsp_compress(lsp_pair_t pair, const void* g, int64_t ldg, lsp_dtype g_dtype, void* s,
+                 lsp_layout s_layout, lsp_stream_t stream) {
+  return guard([&] {
+    require(pair && g && s, "compress: null argument");
+    check_ld(ldg, pair->n, "compress");
+    cudaStream_t st = as_stream(stream);
+    if (s_layout == LSP_LAYOUT_T) {
+      compress_T(*pair, g, ldg, g_dtype, s, st);
+    } else {
+      pair->s_t.ensure(static_cast<size_t>(pair->d) * pair->d * dtype_size(pair->compute));
+      compress_T(*pair, g, ldg, g_dtype, pair->s_t.p, st);
+      launch_transpose(pair->d, pair->d, pair->s_t.p, pair->d, s, pair->d, pair->compute, st);
+    }
+  });
+}
+
+int lsp_decompress(lsp_pair_t pair, const void* s, lsp_layout s_layout, void* out, int64_t ldo,
+                   lsp_dtype out_dtype, lsp_stream_t stream) {
+  return guard([&] {
+    require(pair && s && out, "decompress: null argument");
+    check_ld(ldo, pair->n, "decompress");
+    cudaStream_t st = as_stream(stream);
+    const void* dT = delta_as_T(*pair, s, s_layout, st);
+    launch_decompress(*pair, dT, nullptr, 0, out, ldo, out_dtype, 1.0, 0.0, nullptr, nullptr,
+                      nullptr, st);
+  });
+}
+
+int lsp_decompress_apply(lsp_pair_t pair, const void* delta, lsp_layout delta_layout, double lr,
+                         void* w, int64_t ldw, lsp_dtype w_dtype, lsp_stream_t stream) {
+  return guard([&] {
+    require(pair && delta && w, "decompress_apply: null argument");
+    check_ld(ldw, pair->n, "decompress_apply");
+    cudaStream_t st = as_stream(stream);
+    const void* dT = delta_as_T(*pair, delta, delta_layout, st);
+    launch_decompress(*pair, dT, w, ldw, w, ldw, w_dtype, -lr, 1.0, nullptr, nullptr, nullptr,
+                      st);
+  });
+}
+
+int lsp_estimation_bias(lsp_pair_t pair, const void* sigma, int64_t lds, lsp_dtype dtype,
+                        void* out, int64_t ldo, lsp_stream_t stream) {
+  return guard([&] {
+    require(pair && sigma && out, "estimation_bias: null argument");
+    check_ld(lds, pair->n, "estimation_bias");
+    check_ld(ldo, pair->n, "estimation_bias");
+    cudaStream_t st = as_stream(stream);
+    pair->s_t.ensure(static_cast<size_t>(pair->d) * pair->d * dtype_size(pair->compute));
+    compress_T(*pair, sigma, lds, dtype, pair->s_t.p, st);
+    launch_decompress(*pair, pair->s_t.p, sigma, lds, out, ldo, dtype, 1.0, -1.0, nullptr,
+                      nullptr, nullptr, st);
+  });
+}
+
+int lsp_relative_bias(lsp_pair_t pair, const void* sigma, int64_t lds, lsp_dtype dtype,
+                      double* out, lsp_stream_t stream) {
+  return guard([&] {
+    require(pair && sigma && out, "relative_bias: null argument");
+    check_ld(lds, pair->n, "relative_bias");
+    cudaStream_t st = as_stream(stream);
+    const double den = std::sqrt(sumsq_sync(*pair, pair->m, pair->n, sigma, lds, dtype, st));
+    if (den == 0.0) fail(LSP_EINVAL, "relative_bias: zero sigma");
+    pair->s_t.ensure(static_cast<size_t>(pair->d) * pair->d * dtype_size(pair->compute));
+    compress_T(*pair, sigma, lds, dtype, pair->s_t.p, st);
+    int np = 0;
+    launch_decompress(*pair, pair->s_t.p, sigma, lds, nullptr, 0, dtype, 1.0, -1.0, nullptr,
+                      &pair->red, &np, st);
+    const double num = std::sqrt(reduce_partials_sync(pair->red.as<double>(), np, st));
+    *out = num / den;
+  });
+}
+
+// ---- Adam ------------------------------------------------------------------------
+int lsp_adam_create(int rows, int cols, double beta1, double beta2, double eps,
+                    lsp_dtype compute, lsp_layout layout, lsp_adam_t* out) {
+  return guard([&] {
+    if (rows < 1 || cols < 1) fail(LSP_EINVAL, "make_opt_state: dims must be >= 1");
+    if (beta1 <= 0.0 || beta1 >= 1.0 || beta2 <= 0.0 || beta2 >= 1.0)
+      fail(LSP_EINVAL, "make_opt_state: betas must lie in (0, 1)");
+    if (eps <= 0.0) fail(LSP_EINVAL, "make_opt_state: eps must be positive");
+    require(compute == LSP_F32 || compute == LSP_F64, "adam: compute dtype must be F32 or F64");
+    auto* a = new lsp_adam_s();
+    a->rows = rows;
+    a->cols = cols;
+    a->beta1 = beta1;
+    a->beta2 = beta2;
+    a->eps = eps;
+    a->compute = compute;
+    a->layout = layout;
+    const size_t bytes = a->count() * dtype_size(compute);
+    try {
+      a->m.ensure(bytes);
+      a->v.ensure(bytes);
+      a->flag.ensure(sizeof(int));
+      a->dstep.ensure(sizeof(long long));
+      a->corr.ensure(2 * sizeof(double));
+      LSP_CUDA(cudaMemset(a->m.p, 0, bytes));
+      LSP_CUDA(cudaMemset(a->v.p, 0, bytes));
+      LSP_CUDA(cudaMemset(a->flag.p, 0, sizeof(int)));
+      LSP_CUDA(cudaMemset(a->dstep.p, 0, sizeof(long long)));
+    } catch (...) {
+      delete a;
+      throw;
+    }
+    *out = a;
+  });
+}
+
+int lsp_adam_destroy(lsp_adam_t st) {
+  return guard([&] { delete st; });
+}
+
+int lsp_adam_step(lsp_adam_t a, const void* grad, void* delta, lsp_stream_t stream) {
+  return guard([&] {
+    require(a && grad && delta, "adam_step: null argument");
+    cudaStream_t st = as_stream(stream);
+    // Reference semantics: a non-finite gradient throws before any state
+    // change (subspace_opt.cpp:38) -> check first, skip the update if latched.
+    launch_check_finite(a->count(), grad, a->compute, a->flag.as<int>(), st);
+    launch_adam(*a, grad, delta, a->flag.as<int>(), st);
+  });
+}
+
+int lsp_adam_check(lsp_adam_t a, lsp_stream_t stream) {
+  int rc = guard([&] {
+    require(a != nullptr, "adam_check: null handle");
+    int h = 0;
+    cudaStream_t st = as_stream(stream);
+    LSP_CUDA(cudaMemcpyAsync(&h, a->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    LSP_CUDA(cudaStreamSynchronize(st));
+    if (h) {
+      LSP_CUDA(cudaMemset(a->flag.p, 0, sizeof(int)));
+      fail(LSP_ENUMERIC, "adam_step: non-finite gradient");
+    }
+  });
+  return rc;
+}
+
+int lsp_adam_get(lsp_adam_t a, double* m, double* v, int64_t* step, lsp_layout layout) {
+  return guard([&] {
+    require(a != nullptr, "adam_get: null handle");
+    LSP_CUDA(cudaDeviceSynchronize());
+    LSP_DISPATCH_ACC(a->compute, T, {
+      if (m) moments_to_host<T>(*a, a->m, m, layout);
+      if (v) moments_to_host<T>(*a, a->v, v, layout);
+    })
+    if (step) {
+      long long h = 0;
+      LSP_CUDA(cudaMemcpy(&h, a->dstep.p, sizeof(h), cudaMemcpyDeviceToHost));
+      *step = h;
+    }
+  });
+}
+
+int lsp_adam_set(lsp_adam_t a, const double* m, const double* v, int64_t step,
+                 lsp_layout layout) {
+  return guard([&] {
+    require(a != nullptr, "adam_set: null handle");
+    LSP_CUDA(cudaDeviceSynchronize());
+    LSP_DISPATCH_ACC(a->compute, T, {
+      if (m) moments_from_host<T>(*a, a->m, m, layout);
+      if (v) moments_from_host<T>(*a, a->v, v, layout);
+    })
+    const long long h = step;
+    LSP_CUDA(cudaMemcpy(a->dstep.p, &h, sizeof(h), cudaMemcpyHostToDevice));
+  });
+}
+
+int lsp_adam_info(lsp_adam_t a, int* rows, int* cols, double* beta1, double* beta2,
+                  double* eps) {
+  return guard([&] {
+    require(a != nullptr, "adam_info: null handle");
+    if (rows) *rows = a->rows;
+    if (cols) *cols = a->cols;
+    if (beta1) *beta1 = a->beta1;
+    if (beta2) *beta2 = a->beta2;
+    if (eps) *eps = a->eps;
+  });
+}
+
+// ---- fused per-matrix step -----------------------------------------------------
+static void check_step_args(lsp_pair_t pair, lsp_adam_t a) {
+  require(pair && a, "step: null handle");
+  require(a->rows == pair->d && a->cols == pair->d, "adam_step: grad dims do not match state");
+  require(a->layout == LSP_LAYOUT_T, "step: the Adam state must use LSP_LAYOUT_T");
+  require(a->compute == pair->compute, "step: Adam and pair compute dtypes differ");
+}
+
+static void update_impl(Pair& pr, Adam& a, const void* s_t, void* w, long long ldw,
+                        lsp_dtype w_dtype, double lr, cudaStream_t st) {
+  pr.d_t.ensure(static_cast<size_t>(pr.d) * pr.d * dtype_size(pr.compute));
+  // non-finite S -> skip Adam and the apply (NumericError semantics)
+  launch_check_finite(a.count(), s_t, a.compute, a.flag.as<int>(), st);
+  launch_adam(a, s_t, pr.d_t.p, a.flag.as<int>(), st);
+  launch_decompress(pr, pr.d_t.p, w, ldw, w, ldw, w_dtype, -lr, 1.0, a.flag.as<int>(), nullptr,
+                    nullptr, st);
+}
+
+int lsp_step(lsp_pair_t pair, lsp_adam_t a, const void* g, int64_t ldg, lsp_dtype g_dtype,
+             void* w, int64_t ldw, lsp_dtype w_dtype, double lr, void* s_out,
+             lsp_stream_t stream) {
+  return guard([&] {
+    check_step_args(pair, a);
+    require(g && w, "step: null argument");
+    check_ld(ldg, pair->n, "step");
+    check_ld(ldw, pair->n, "step");
+    cudaStream_t st = as_stream(stream);
+    void* s_t = s_out;
+    if (!s_t) {
+      pair->s_t.ensure(static_cast<size_t>(pair->d) * pair->d * dtype_size(pair->compute));
+      s_t = pair->s_t.p;
+    }
+    compress_T(*pair, g, ldg, g_dtype, s_t, st);
+    update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, st);
+  });
+}
+
+int lsp_update(lsp_pair_t pair, lsp_adam_t a, const void* s_t, void* w, int64_t ldw,
+               lsp_dtype w_dtype, double lr, lsp_stream_t stream) {
+  return guard([&] {
+    check_step_args(pair, a);
+    require(s_t && w, "update: null argument");
+    check_ld(ldw, pair->n, "update");
+    update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, as_stream(stream));
+  });
+}
+
+}  // extern "C"

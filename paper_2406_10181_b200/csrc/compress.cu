@@ -1,0 +1,299 @@
+// Compress: S = P^T G Q  (reference: proj/src/projector.cpp:119-168).
+//
+// Two stages, both written for HBM-bound streaming on sm_100a:
+//
+//  stage 1  Z^T = G^T P  (n x d).  One CTA owns a band of 32 columns of G and
+//           every subspace bin (32 bins per warp, accumulators in registers:
+//           lane = column, register = bin).  G is streamed ONCE, row chunk by
+//           row chunk, through a cp.async double buffer; the chunk-major CSC
+//           table of P says which tile rows feed which bin, so every G element
+//           is read from HBM once and from shared memory k times (conflict-
+//           free: a warp reads one 32-wide tile row).  No atomics, fixed
+//           summation order -> bitwise deterministic.
+//  stage 2  S^T[b][:] = sum_{j in CSC_Q(b)} q_jb Z^T[j][:]  -- coalesced row
+//           gathers of the L2-resident Z^T (k_gather).
+#include <algorithm>
+
+#include "core.cuh"
+
+namespace lspb {
+
+namespace {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Load rows [row0, row0+BM) x cols [j0, j0+32) of G into a BM x 32 tile.
+// Rows >= m are skipped (never referenced); columns >= n are zero-filled.
+template <typename Tin, int BM, int NT>
+__device__ __forceinline__ void load_tile(Tin* tile, const Tin* __restrict__ g, long long ldg,
+                                          int m, int n, int row0, int j0, bool vec) {
+  constexpr int kPer16 = 16 / sizeof(Tin);       // elements per 16 B
+  constexpr int kPieces = 32 / kPer16;           // 16 B pieces per tile row
+  const int tid = threadIdx.x;
+  if (vec) {
+#pragma unroll 4
+    for (int p = tid; p < BM * kPieces; p += NT) {
+      const int row = p / kPieces, piece = p % kPieces;
+      const int gr = row0 + row, gc = j0 + piece * kPer16;
+      if (gr >= m) continue;
+      const int valid = min(kPer16, n - gc);
+      const Tin* src = g + static_cast<long long>(gr) * ldg + (valid > 0 ? gc : 0);
+      cp_async16(tile + row * 32 + piece * kPer16, src, valid > 0 ? valid * (int)sizeof(Tin) : 0);
+    }
+  } else {
+    for (int p = tid; p < BM * 32; p += NT) {
+      const int row = p >> 5, col = p & 31;
+      const int gr = row0 + row, gc = j0 + col;
+      if (gr >= m) continue;
+      tile[p] = gc < n ? g[static_cast<long long>(gr) * ldg + gc] : Tin(0.0f);
+    }
+  }
+}
+
+template <typename Tin, typename Tacc, int WARPS, int BM>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    k_compress_stage1(const Tin* __restrict__ g, long long ldg, int m, int n, int d,
+                      const int* __restrict__ split,
+                      const typename EntryOf<Tacc>::type* __restrict__ ent, int nchunks,
+                      Tacc* __restrict__ zt, int ldz, int vec) {
+  constexpr int NT = WARPS * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tin* tiles = reinterpret_cast<Tin*>(smem_raw);  // [2][BM][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * 32;
+  const int bin0 = blockIdx.y * NT + warp * 32;
+  const int my_bin = bin0 + lane;
+  const bool vec16 = vec != 0;
+
+  Tacc acc[32];
+#pragma unroll
+  for (int b = 0; b < 32; ++b) acc[b] = Tacc(0);
+
+  load_tile<Tin, BM, NT>(tiles, g, ldg, m, n, 0, j0, vec16);
+  cp_async_commit();
+  for (int c = 0; c < nchunks; ++c) {
+    // Chunk c+1 goes to the other buffer; the barrier below the wait also
+    // guarantees every warp has finished reading it (chunk c-1).
+    cp_async_wait<0>();
+    __syncthreads();
+    if (c + 1 < nchunks)
+      load_tile<Tin, BM, NT>(tiles + ((c + 1) & 1) * BM * 32, g, ldg, m, n, (c + 1) * BM, j0,
+                             vec16);
+    cp_async_commit();
+    const Tin* t = tiles + (c & 1) * BM * 32 + lane;
+    // Entries of (chunk c, bin) are contiguous and bins follow each other, so
+    // bin b's range is [end(b-1), end(b)).
+    const long long base = static_cast<long long>(c) * d;
+    int e = split[base + min(bin0, d)];
+    const int my_end = split[base + min(my_bin + 1, d)];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const int end = __shfl_sync(0xffffffffu, my_end, b);
+      Tacc a = acc[b];
+      for (; e < end; ++e) {
+        const auto en = ent[e];
+        a = fma(en.val, cvt<Tacc>(t[en.off]), a);
+      }
+      acc[b] = a;
+    }
+  }
+  const int j = j0 + lane;
+  if (j < n) {
+    Tacc* dst = zt + static_cast<long long>(j) * ldz + bin0;
+    if (bin0 + 32 <= ldz && (ldz % 4) == 0 && sizeof(Tacc) == 4) {
+#pragma unroll
+      for (int b = 0; b < 32; b += 4)
+        *reinterpret_cast<float4*>(dst + b) =
+            make_float4((float)acc[b], (float)acc[b + 1], (float)acc[b + 2], (float)acc[b + 3]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < 32; ++b)
+        if (bin0 + b < ldz) dst[b] = acc[b];
+    }
+  }
+}
+
+template <typename Tin, typename Tacc, int WARPS>
+void stage1_impl(const Pair& pr, const Tin* g, long long ldg, Tacc* zt, cudaStream_t st) {
+  constexpr int kStageBytes = WARPS >= 16 ? 65536 : 32768;
+  constexpr int BM = kStageBytes / (32 * sizeof(Tin));
+  Projector& P = *pr.p;
+  const ChunkTable& ct = P.chunk_table(BM);
+  const int bins_per_cta = WARPS * 32;
+  dim3 grid(ceil_div(pr.n, 32), ceil_div(pr.d, bins_per_cta));
+  const int smem = 2 * BM * 32 * sizeof(Tin);
+  auto kern = k_compress_stage1<Tin, Tacc, WARPS, BM>;
+  LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const bool vec = (reinterpret_cast<uintptr_t>(g) % 16 == 0) && ((ldg * sizeof(Tin)) % 16 == 0);
+  kern<<<grid, WARPS * 32, smem, st>>>(g, ldg, pr.m, pr.n, pr.d, ct.split.as<int>(),
+                                        ct.ent.as<typename EntryOf<Tacc>::type>(), ct.nchunks,
+                                        zt, pr.ldz(), vec ? 1 : 0);
+  after_launch("compress_stage1");
+}
+
+}  // namespace
+
+void launch_compress_stage1(const Pair& pr, const void* g, long long ldg, lsp_dtype gdt,
+                            void* zt, cudaStream_t st) {
+  LSP_DISPATCH_ACC(pr.compute, Tacc, {
+    LSP_DISPATCH_STORAGE(gdt, Tin, {
+      const int need = ceil_div(pr.d, 32);  // warps needed to cover every bin once
+      constexpr int kMaxWarps = sizeof(Tacc) == 8 ? 16 : 32;
+      if constexpr (kMaxWarps == 32) {
+        if (need > 16) {
+          stage1_impl<Tin, Tacc, 32>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+          break;
+        }
+      }
+      if (need > 8)
+        stage1_impl<Tin, Tacc, 16>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+      else if (need > 4)
+        stage1_impl<Tin, Tacc, 8>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+      else
+        stage1_impl<Tin, Tacc, 4>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+    })
+  })
+}
+
+// ---------------------------------------------------------------------------
+// Row gather: out[r][:] = beta*in[r][:] + alpha * sum_t val[t] * src[idx[t]][:]
+// One warp per output row; lanes stride the columns 32 at a time, 8 columns in
+// flight per lane.  Optional deterministic per-block sum of squares of the
+// result (for Frobenius norms).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kGatherWarps = 8;
+constexpr int kGatherUnroll = 8;
+
+template <typename Tsrc, typename Tdst, typename Tacc>
+__global__ void __launch_bounds__(kGatherWarps * 32)
+    k_gather(int R, int c, const int* __restrict__ ptr, int k, const int* __restrict__ idx,
+             const Tacc* __restrict__ val, const Tsrc* __restrict__ src, long long lds,
+             const Tdst* in, long long ldi, Tdst* out, long long ldo, Tacc alpha, Tacc beta,
+             double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double ss = 0.0;
+  for (int r = blockIdx.x * kGatherWarps + warp; r < R; r += gridDim.x * kGatherWarps) {
+    const int e0 = ptr ? ptr[r] : r * k;
+    const int e1 = ptr ? ptr[r + 1] : e0 + k;
+    for (int c0 = 0; c0 < c; c0 += 32 * kGatherUnroll) {
+      Tacc acc[kGatherUnroll];
+#pragma unroll
+      for (int u = 0; u < kGatherUnroll; ++u) acc[u] = Tacc(0);
+      for (int e = e0; e < e1; ++e) {
+        const Tacc v = val[e];
+        const Tsrc* s = src + static_cast<long long>(idx[e]) * lds;
+#pragma unroll
+        for (int u = 0; u < kGatherUnroll; ++u) {
+          const int col = c0 + u * 32 + lane;
+          if (col < c) acc[u] = fma(v, cvt<Tacc>(s[col]), acc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGatherUnroll; ++u) {
+        const int col = c0 + u * 32 + lane;
+        if (col >= c) continue;
+        Tacc res = alpha * acc[u];
+        if (in && beta != Tacc(0))
+          res = fma(beta, cvt<Tacc>(in[static_cast<long long>(r) * ldi + col]), res);
+        if (out) out[static_cast<long long>(r) * ldo + col] = cvt<Tdst>(res);
+        if (partials) ss += static_cast<double>(res) * static_cast<double>(res);
+      }
+    }
+  }
+  if (partials) {
+    __shared__ double red[kGatherWarps];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kGatherWarps; ++w) t += red[w];
+      partials[blockIdx.x] = t;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const void* val,
+                   lsp_dtype acc, const void* src, long long lds, lsp_dtype src_dt,
+                   const void* in, long long ldi, void* out, long long ldo, lsp_dtype out_dt,
+                   double alpha, double beta, DevBuf* partials, int* nparts, cudaStream_t st) {
+  if (R <= 0 || c <= 0) {
+    if (nparts) *nparts = 0;
+    return;
+  }
+  const int grid = std::min(ceil_div(R, kGatherWarps), 8 * num_sms());
+  if (nparts) *nparts = grid;
+  if (partials) partials->ensure(static_cast<size_t>(grid) * sizeof(double));
+  double* parts = partials ? partials->as<double>() : nullptr;
+  LSP_DISPATCH_ACC(acc, Tacc, {
+    LSP_DISPATCH_STORAGE(src_dt, Tsrc, {
+      LSP_DISPATCH_STORAGE(out_dt, Tdst, {
+        k_gather<Tsrc, Tdst, Tacc><<<grid, kGatherWarps * 32, 0, st>>>(
+            R, c, ptr, k, idx, static_cast<const Tacc*>(val), static_cast<const Tsrc*>(src), lds,
+            static_cast<const Tdst*>(in), ldi, static_cast<Tdst*>(out), ldo,
+            static_cast<Tacc>(alpha), static_cast<Tacc>(beta), parts);
+      })
+    })
+  })
+  after_launch("gather");
+}
+
+// ---------------------------------------------------------------------------
+// Tiled transpose dst[c][r] = src[r][c] (32x32 tiles through padded smem).
+// ---------------------------------------------------------------------------
+namespace {
+template <typename T>
+__global__ void k_transpose(int rows, int cols, const T* __restrict__ src, long long lds,
+                            T* __restrict__ dst, long long ldd) {
+  __shared__ T tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = by + y, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[y][threadIdx.x] = src[static_cast<long long>(r) * lds + c];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int c = bx + y, r = by + threadIdx.x;
+    if (r < rows && c < cols) dst[static_cast<long long>(c) * ldd + r] = tile[threadIdx.x][y];
+  }
+}
+}  // namespace
+
+void launch_transpose(int rows, int cols, const void* src, long long lds, void* dst,
+                      long long ldd, lsp_dtype dt, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32)), block(32, 8);
+  LSP_DISPATCH_STORAGE(dt, T, {
+    k_transpose<T><<<grid, block, 0, st>>>(rows, cols, static_cast<const T*>(src), lds,
+                                           static_cast<T*>(dst), ldd);
+  })
+  after_launch("transpose");
+}
+
+// S^T = Q^T (G^T P): stage 1 into pr.zt, stage 2 gather into s_t (d x d, ld d).
+void compress_T(Pair& pr, const void* g, long long ldg, lsp_dtype gdt, void* s_t,
+                cudaStream_t st) {
+  const size_t vs = dtype_size(pr.compute);
+  pr.zt.ensure(static_cast<size_t>(pr.n) * pr.ldz() * vs);
+  launch_compress_stage1(pr, g, ldg, gdt, pr.zt.p, st);
+  const Projector& Q = *pr.q;
+  launch_gather(pr.d, pr.d, Q.csc_ptr.as<int>(), 0, Q.csc_row.as<int>(), Q.csc_val.p,
+                pr.compute, pr.zt.p, pr.ldz(), pr.compute, nullptr, 0, s_t, pr.d, pr.compute,
+                1.0, 0.0, nullptr, nullptr, st);
+}
+
+}  // namespace lspb

@@ -1,0 +1,146 @@
+// Internal handle types and kernel launchers.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace lspb {
+
+// Owning device allocation (move-only).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // Grow-only reallocation (contents are not preserved).
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    release();
+    LSP_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Entry of the chunk-major stage-1 table: tile offset (row_in_chunk * 32) and value.
+struct EntryF {
+  int32_t off;
+  float val;
+};
+struct __align__(16) EntryD {
+  int32_t off;
+  int32_t pad;
+  double val;
+};
+template <typename Tacc>
+struct EntryOf;
+template <>
+struct EntryOf<float> {
+  using type = EntryF;
+};
+template <>
+struct EntryOf<double> {
+  using type = EntryD;
+};
+
+struct ChunkTable {
+  int bm = 0;
+  int nchunks = 0;
+  DevBuf split;  // int32 [nchunks*d + 1]
+  DevBuf ent;    // EntryF / EntryD [nnz]
+  DevBuf perm;   // int32 [nnz] -> CSR index (for value refresh)
+};
+
+// Device-resident SparseProjector (proj/include/lsp/projector.hpp:18-30) in
+// CSR (row-major positions/values, the reference layout) and CSC orientation.
+struct Projector {
+  int n_rows = 0, d = 0, r = 0;
+  lsp_dtype compute = LSP_F32;
+  std::vector<int32_t> h_pos;
+  std::vector<double> h_val;
+  std::vector<int32_t> h_csc_ptr, h_csc_rows, h_csc_perm;
+  DevBuf pos, val;                           // CSR: int32 / compute [n_rows*r]
+  DevBuf csc_ptr, csc_row, csc_val, csc_perm;  // CSC: [d+1], [nnz], [nnz], [nnz]
+  std::vector<std::unique_ptr<ChunkTable>> chunks;
+
+  size_t nnz() const { return static_cast<size_t>(n_rows) * r; }
+  size_t vsize() const { return dtype_size(compute); }
+  const ChunkTable& chunk_table(int bm);
+  // Re-derive CSC and chunk-table values from the CSR values on the device.
+  void refresh_values(cudaStream_t st);
+  void upload_values();  // h_val -> device CSR values, then refresh
+};
+
+struct Pair {
+  Projector* p = nullptr;
+  Projector* q = nullptr;
+  int m = 0, n = 0, d = 0;
+  lsp_dtype compute = LSP_F32;
+  DevBuf zt;    // n x ldz, compute   (stage-1 output Z^T = G^T P)
+  DevBuf s_t;   // d x d,  compute    (S^T)
+  DevBuf d_t;   // d x d,  compute    (delta^T or transposed input)
+  DevBuf red;   // double partial sums
+  DevBuf flag;  // int
+  int ldz() const { return static_cast<int>(round_up(d, 4)); }
+  int* flag_ptr();
+};
+
+struct Adam {
+  int rows = 0, cols = 0;
+  double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  lsp_dtype compute = LSP_F32;
+  lsp_layout layout = LSP_LAYOUT_T;
+  DevBuf m, v;
+  DevBuf flag;   // int: latched non-finite gradient
+  DevBuf dstep;  // int64: step counter, advanced on the device (graph-replay safe)
+  DevBuf corr;   // double[2]: bias corrections (1-b1^t, 1-b2^t) of the current step
+  size_t count() const { return static_cast<size_t>(rows) * cols; }
+};
+
+// ---- launchers (templated kernels live in the .cu files) -------------------
+// Z^T = G^T P (n x ldz) with the chunked register-accumulator kernel.
+void launch_compress_stage1(const Pair& pr, const void* g, long long ldg, lsp_dtype gdt,
+                            void* zt, cudaStream_t st);
+// out[r][:] = beta*in[r][:] + alpha * sum_t val[t] * src[idx[t]][:]
+// Rows' entries are [ptr[r], ptr[r+1]) when ptr != nullptr, else [r*k, r*k+k).
+void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const void* val,
+                   lsp_dtype acc, const void* src, long long lds, lsp_dtype src_dt,
+                   const void* in, long long ldi, void* out, long long ldo, lsp_dtype out_dt,
+                   double alpha, double beta, DevBuf* partials, int* nparts, cudaStream_t st);
+void launch_transpose(int rows, int cols, const void* src, long long lds, void* dst,
+                      long long ldd, lsp_dtype dt, cudaStream_t st);
+// Fused decompress: out = beta*in + alpha * P (delta) Q^T, delta given as delta^T.
+void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long long ldi,
+                       void* out, long long ldo, lsp_dtype dt, double alpha, double beta,
+                       const int* skip_flag, DevBuf* partials, int* nparts, cudaStream_t st);
+void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st);
+void launch_check_finite(size_t cnt, const void* x, lsp_dtype dt, int* flag, cudaStream_t st);
+void launch_convert(size_t cnt, const void* src, lsp_dtype sdt, void* dst, lsp_dtype ddt,
+                    cudaStream_t st);
+void launch_convert2d(int rows, int cols, const void* src, long long lds, lsp_dtype sdt,
+                      void* dst, long long ldd, lsp_dtype ddt, cudaStream_t st);
+// deterministic sum of `n` doubles on device -> host value (synchronous)
+double reduce_partials_sync(const double* partials, int n, cudaStream_t st);
+double sumsq_sync(Pair& pr, int rows, int cols, const void* x, long long ld, lsp_dtype dt,
+                  cudaStream_t st);
+void launch_refresh_values(const Projector& p, cudaStream_t st);
+
+// High-level building blocks used by the C-ABI.
+void compress_T(Pair& pr, const void* g, long long ldg, lsp_dtype gdt, void* s_t,
+                cudaStream_t st);
+const void* delta_as_T(Pair& pr, const void* s, lsp_layout layout, cudaStream_t st);
+
+}  // namespace lspb

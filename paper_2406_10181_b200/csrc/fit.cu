@@ -1,0 +1,570 @@
+// Projector fit (Eq. 3) and optimizer-state transfer, on the device in fp64.
+//
+// Reference: fit_loss / fit_gradient / fit  proj/src/projector.cpp:189-315,
+//            projector_gram / reproject_state proj/src/subspace_opt.cpp:59-101.
+//
+// The reference materialises the m x n bias B = P S Q^T - G and dense m x d,
+// n x d products (O((m+n) d^2) per target, 19.7 s at 2048x5504, d=1024).  Here
+// every product is factored through the sparse projectors, so nothing larger
+// than max(m,n) x d is formed and no dense d^3 GEMM is needed:
+//   S   = P^T G Q                          (compress, stage 1 + 2)
+//   A1  = Gp S = P^T (P S)                 (two row gathers)
+//   V   = Q A1^T = (A1 Q^T)^T
+//   D   = Gp S Gq - 2 S ,  D^T = Q^T V - 2 S^T
+//   |B|^2 = <D, S> + |G|^2                 (since P^T G Q = S)
+//   dL/dP(i,a) = 2/T [ (P A2)[i,:] . S[a,:]  + X[i,:] . D[a,:] ],  A2 = S Gq, X = G Q
+//   dL/dQ(j,b) = 2/T [ V[j,:] . S^T[b,:]     + Z^T[j,:] . D^T[b,:] ], Z^T = G^T P
+// (derivation in DESIGN.md).  Everything runs in fp64 on shadow fp64 copies of
+// the projectors; the fitted values are written back to the pair at the end.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "core.cuh"
+#include "host_projector.h"
+
+struct lsp_projector_s : lspb::Projector {};
+struct lsp_pair_s : lspb::Pair {};
+struct lsp_adam_s : lspb::Adam {};
+
+namespace lspb {
+extern thread_local std::string g_last_error;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+constexpr int kRedBlocks = 512;
+
+// Deterministic per-block partial dot products <a, b> over `cnt` elements.
+__global__ void k_dot(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ partials) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 256; ++i) t += red[i];
+    partials[blockIdx.x] = t;
+  }
+}
+
+// grad[r*k + l] += scale * ( A1[r,:].B1[pos[r*k+l],:] + A2[r,:].B2[pos[r*k+l],:] )
+__global__ void k_sddmm(int R, int k, int d, const int* __restrict__ pos,
+                        const double* __restrict__ A1, const double* __restrict__ B1,
+                        const double* __restrict__ A2, const double* __restrict__ B2, int ld,
+                        double scale, double* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < R; r += gridDim.x * warps) {
+    const double* a1 = A1 + static_cast<long long>(r) * ld;
+    const double* a2 = A2 + static_cast<long long>(r) * ld;
+    for (int l = 0; l < k; ++l) {
+      const int b = pos[static_cast<long long>(r) * k + l];
+      const double* b1 = B1 + static_cast<long long>(b) * ld;
+      const double* b2 = B2 + static_cast<long long>(b) * ld;
+      double s = 0.0;
+      for (int c = lane; c < d; c += 32) s = fma(a1[c], b1[c], fma(a2[c], b2[c], s));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) grad[static_cast<long long>(r) * k + l] += scale * s;
+    }
+  }
+}
+
+// out (da x db, row-major) = A^T B for two projectors over the same rows, in
+// the reference's summation order (rows ascending per output entry,
+// subspace_opt.cpp:59-70), without contraction so fp64 results match it.
+template <typename Ta, typename Tb>
+__global__ void k_gram(int da, int db, int rb, const int* __restrict__ a_csc_ptr,
+                       const int* __restrict__ a_csc_row, const Ta* __restrict__ a_csc_val,
+                       const int* __restrict__ b_pos, const Tb* __restrict__ b_val,
+                       double* __restrict__ out) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < da; x += gridDim.x * blockDim.x) {
+    double* orow = out + static_cast<long long>(x) * db;
+    for (int t = a_csc_ptr[x]; t < a_csc_ptr[x + 1]; ++t) {
+      const int i = a_csc_row[t];
+      const double va = static_cast<double>(a_csc_val[t]);
+      for (int kb = 0; kb < rb; ++kb) {
+        const long long e = static_cast<long long>(i) * rb + kb;
+        const int y = b_pos[e];
+        orow[y] = __dadd_rn(orow[y], __dmul_rn(va, static_cast<double>(b_val[e])));
+      }
+    }
+  }
+}
+
+// Tiled fp64 GEMM C = A (MxK) * B (KxN), row-major, fixed k order.
+constexpr int kGT = 64, kGK = 16;
+__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double* __restrict__ A,
+                                               const double* __restrict__ B, double* __restrict__ C) {
+  __shared__ double As[kGK][kGT + 1];
+  __shared__ double Bs[kGK][kGT + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int row0 = blockIdx.y * kGT, col0 = blockIdx.x * kGT;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += kGK) {
+    for (int t = threadIdx.x; t < kGT * kGK; t += 256) {
+      const int r = t / kGK, c = t % kGK;  // A tile: rows row0+r, k k0+c
+      As[c][r] = (row0 + r < M && k0 + c < K) ? A[static_cast<long long>(row0 + r) * K + k0 + c] : 0.0;
+      const int kr = t / kGT, cc = t % kGT;  // B tile: k k0+kr, cols col0+cc
+      Bs[kr][cc] = (k0 + kr < K && col0 + cc < N) ? B[static_cast<long long>(k0 + kr) * N + col0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = row0 + ty * 4 + i, c = col0 + tx * 4 + j;
+      if (r < M && c < N) C[static_cast<long long>(r) * N + c] = acc[i][j];
+    }
+}
+
+__global__ void k_square(long long cnt, double* __restrict__ x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = x[i] * x[i];
+}
+__global__ void k_clamp0(long long cnt, double* __restrict__ x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    if (x[i] < 0.0) x[i] = 0.0;
+}
+
+int egrid(long long cnt) {
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((cnt + 255) / 256, 4096)));
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+double dot_sync(const double* a, const double* b, long long cnt, DevBuf& parts, cudaStream_t st) {
+  parts.ensure(kRedBlocks * sizeof(double));
+  k_dot<<<kRedBlocks, 256, 0, st>>>(cnt, a, b, parts.as<double>());
+  after_launch("dot");
+  return reduce_partials_sync(parts.as<double>(), kRedBlocks, st);
+}
+
+void dgemm(int M, int N, int K, const double* A, const double* B, double* C, cudaStream_t st) {
+  dim3 grid(ceil_div(N, kGT), ceil_div(M, kGT));
+  k_dgemm<<<grid, 256, 0, st>>>(M, N, K, A, B, C);
+  after_launch("dgemm");
+}
+
+// out = alpha * (rows of src gathered by the CSR of P) [+ beta*in]
+void csr_gather(const Projector& P, const double* src, int c, double* out,
+                cudaStream_t st, double beta = 0.0, const double* in = nullptr) {
+  launch_gather(P.n_rows, c, nullptr, P.r, P.pos.as<int>(), P.val.p, LSP_F64, src, c, LSP_F64,
+                in, c, out, c, LSP_F64, 1.0, beta, nullptr, nullptr, st);
+}
+void csc_gather(const Projector& P, const double* src, int c, double* out,
+                cudaStream_t st, double beta = 0.0, const double* in = nullptr) {
+  launch_gather(P.d, c, P.csc_ptr.as<int>(), 0, P.csc_row.as<int>(), P.csc_val.p, LSP_F64, src,
+                c, LSP_F64, in, c, out, c, LSP_F64, 1.0, beta, nullptr, nullptr, st);
+}
+
+std::unique_ptr<lsp_projector_s> shadow64(const Projector& P, const std::vector<double>& vals) {
+  auto S = std::make_unique<lsp_projector_s>();
+  S->n_rows = P.n_rows;
+  S->d = P.d;
+  S->r = P.r;
+  S->compute = LSP_F64;
+  S->h_pos = P.h_pos;
+  S->h_val = vals;
+  S->h_csc_ptr = P.h_csc_ptr;
+  S->h_csc_rows = P.h_csc_rows;
+  S->h_csc_perm = P.h_csc_perm;
+  const size_t nnz = P.nnz();
+  auto up = [](DevBuf& b, const void* src, size_t bytes) {
+    b.ensure(std::max<size_t>(bytes, 16));
+    if (bytes) LSP_CUDA(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
+  };
+  up(S->pos, S->h_pos.data(), nnz * 4);
+  up(S->csc_ptr, S->h_csc_ptr.data(), S->h_csc_ptr.size() * 4);
+  up(S->csc_row, S->h_csc_rows.data(), nnz * 4);
+  up(S->csc_perm, S->h_csc_perm.data(), nnz * 4);
+  S->csc_val.ensure(std::max<size_t>(nnz * 8, 16));
+  up(S->val, vals.data(), nnz * 8);
+  launch_refresh_values(*S, nullptr);
+  return S;
+}
+
+void set_values64(Projector& S, const std::vector<double>& vals, cudaStream_t st) {
+  S.h_val = vals;
+  LSP_CUDA(cudaMemcpyAsync(S.val.p, vals.data(), vals.size() * 8, cudaMemcpyHostToDevice, st));
+  launch_refresh_values(S, st);
+}
+
+// The fit engine: fp64 shadows of (P, Q), the targets and their transposes.
+struct FitEngine {
+  Pair& orig;
+  int m, n, d, r, T;
+  cudaStream_t st;
+  std::unique_ptr<lsp_projector_s> P, Q;
+  lsp_pair_s pq;   // (P, Q): stage 1 on G -> Z^T
+  lsp_pair_s qp;   // (Q, P): stage 1 on G^T -> X
+  std::vector<DevBuf> g, gT;  // fp64 targets and transposes
+  std::vector<double> gnorm2;
+  DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, parts;
+
+  FitEngine(Pair& pr, const void* const* targets, int t, long long ld, lsp_dtype dt,
+            cudaStream_t stream)
+      : orig(pr), m(pr.m), n(pr.n), d(pr.d), r(pr.p->r), T(t), st(stream) {
+    require(t >= 1, "fit: empty target corpus");
+    require(pr.p->r == pr.q->r, "fit: P and Q must have the same nonzeros per row");
+    require(ld >= n, "fit: target leading dimension smaller than columns");
+    P = shadow64(*pr.p, pr.p->h_val);
+    Q = shadow64(*pr.q, pr.q->h_val);
+    pq.p = P.get(), pq.q = Q.get(), pq.m = m, pq.n = n, pq.d = d, pq.compute = LSP_F64;
+    qp.p = Q.get(), qp.q = P.get(), qp.m = n, qp.n = m, qp.d = d, qp.compute = LSP_F64;
+    const size_t mn = static_cast<size_t>(m) * n;
+    g.resize(t);
+    gT.resize(t);
+    gnorm2.resize(t);
+    for (int i = 0; i < t; ++i) {
+      require(targets[i] != nullptr, "fit: null target");
+      g[i].ensure(mn * 8);
+      gT[i].ensure(mn * 8);
+      // dense fp64 copy (handles ld and dtype), then its transpose
+      launch_convert2d(m, n, targets[i], ld, dt, g[i].p, n, LSP_F64, st);
+      launch_transpose(m, n, g[i].p, n, gT[i].p, m, LSP_F64, st);
+      gnorm2[i] = dot_sync(g[i].as<double>(), g[i].as<double>(), static_cast<long long>(mn), parts, st);
+    }
+    const size_t dd2 = static_cast<size_t>(d) * d * 8;
+    for (DevBuf* b : {&sT, &s, &a1, &a1T, &dT, &dd, &a2T, &a2}) b->ensure(dd2);
+    const size_t ms = static_cast<size_t>(m) * d * 8, ns = static_cast<size_t>(n) * d * 8;
+    u.ensure(ms);
+    w1.ensure(ms);
+    v.ensure(ns);
+    qs.ensure(ns);
+  }
+
+  void set_values(const std::vector<double>& pv, const std::vector<double>& qv) {
+    set_values64(*P, pv, st);
+    set_values64(*Q, qv, st);
+  }
+
+  // S^T (and Z^T in pq.zt) for target i, then D^T; returns |b_i|^2.
+  double eval_target(int i) {
+    compress_T(pq, g[i].p, n, LSP_F64, sT.p, st);
+    launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);
+    csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S     (m x d)
+    csc_gather(*P, u.as<double>(), d, a1.as<double>(), st);        // A1 = P^T U   (d x d)
+    launch_transpose(d, d, a1.p, d, a1T.p, d, LSP_F64, st);
+    csr_gather(*Q, a1T.as<double>(), d, v.as<double>(), st);       // V  = Q A1^T  (n x d)
+    csc_gather(*Q, v.as<double>(), d, dT.as<double>(), st, -2.0, sT.as<double>());  // D^T
+    const double sd = dot_sync(dT.as<double>(), sT.as<double>(), static_cast<long long>(d) * d, parts, st);
+    return std::max(0.0, sd + gnorm2[i]);
+  }
+
+  // loss = mean_t |b_t|^2 + reg ; rel = mean over nonzero targets of |b_t|/|G_t|
+  void loss(const std::vector<double>& pv, const std::vector<double>& qv,
+            const lsp_fit_config& cfg, double* loss_out, double* rel_out) {
+    set_values(pv, qv);
+    double sum = 0.0, rel = 0.0;
+    int counted = 0;
+    for (int i = 0; i < T; ++i) {
+      const double b2 = eval_target(i);
+      sum += b2;
+      if (gnorm2[i] > 0.0) {
+        rel += std::sqrt(b2) / std::sqrt(gnorm2[i]);
+        ++counted;
+      }
+    }
+    *loss_out = sum / T + reg_term(pv, qv, cfg);
+    if (rel_out) *rel_out = counted ? rel / counted : 0.0;
+  }
+
+  static double reg_term(const std::vector<double>& pv, const std::vector<double>& qv,
+                         const lsp_fit_config& cfg) {
+    if (cfg.reg_beta == 0.0) return 0.0;
+    double ps = 0.0, qs2 = 0.0;
+    for (double x : pv) ps += x * x;
+    for (double x : qv) qs2 += x * x;
+    if (cfg.reg_kind == LSP_REG_SQUARED) return cfg.reg_beta * (ps + qs2);
+    return cfg.reg_beta * (std::sqrt(ps) + std::sqrt(qs2));
+  }
+
+  void gradient(const std::vector<double>& pv, const std::vector<double>& qv,
+                const lsp_fit_config& cfg, std::vector<double>& gp, std::vector<double>& gq) {
+    set_values(pv, qv);
+    DevBuf dgp, dgq;
+    dgp.ensure(std::max<size_t>(pv.size() * 8, 16));
+    dgq.ensure(std::max<size_t>(qv.size() * 8, 16));
+    LSP_CUDA(cudaMemsetAsync(dgp.p, 0, pv.size() * 8, st));
+    LSP_CUDA(cudaMemsetAsync(dgq.p, 0, qv.size() * 8, st));
+    x.ensure(static_cast<size_t>(m) * qp.ldz() * 8);
+    const double scale = 2.0 / T;
+    for (int i = 0; i < T; ++i) {
+      eval_target(i);                                               // S^T, Z^T (pq.zt), A1, V, D^T
+      launch_transpose(d, d, dT.p, d, dd.p, d, LSP_F64, st);        // D
+      launch_compress_stage1(qp, gT[i].p, m, LSP_F64, x.p, st);     // X = G Q  (m x ldz)
+      csr_gather(*Q, sT.as<double>(), d, qs.as<double>(), st);      // Q S^T    (n x d)
+      csc_gather(*Q, qs.as<double>(), d, a2T.as<double>(), st);     // A2^T = Gq S^T
+      launch_transpose(d, d, a2T.p, d, a2.p, d, LSP_F64, st);       // A2 = S Gq
+      csr_gather(*P, a2.as<double>(), d, w1.as<double>(), st);      // W1 = P A2 (m x d)
+      // X and Z^T have leading dimension ldz (= round_up(d,4)); compact them to d.
+      const double* xd = x.as<double>();
+      const double* zd = pq.zt.as<double>();
+      DevBuf xc, zc;
+      if (qp.ldz() != d) {
+        xc.ensure(static_cast<size_t>(m) * d * 8);
+        zc.ensure(static_cast<size_t>(n) * d * 8);
+        launch_convert2d(m, d, xd, qp.ldz(), LSP_F64, xc.p, d, LSP_F64, st);
+        launch_convert2d(n, d, zd, pq.ldz(), LSP_F64, zc.p, d, LSP_F64, st);
+        xd = xc.as<double>();
+        zd = zc.as<double>();
+      }
+      k_sddmm<<<egrid(static_cast<long long>(m) * 32), 256, 0, st>>>(
+          m, r, d, P->pos.as<int>(), w1.as<double>(), s.as<double>(), xd, dd.as<double>(), d,
+          scale, dgp.as<double>());
+      after_launch("sddmm_p");
+      k_sddmm<<<egrid(static_cast<long long>(n) * 32), 256, 0, st>>>(
+          n, r, d, Q->pos.as<int>(), v.as<double>(), sT.as<double>(), zd, dT.as<double>(), d,
+          scale, dgq.as<double>());
+      after_launch("sddmm_q");
+      LSP_CUDA(cudaStreamSynchronize(st));
+    }
+    gp.resize(pv.size());
+    gq.resize(qv.size());
+    LSP_CUDA(cudaMemcpyAsync(gp.data(), dgp.p, gp.size() * 8, cudaMemcpyDeviceToHost, st));
+    LSP_CUDA(cudaMemcpyAsync(gq.data(), dgq.p, gq.size() * 8, cudaMemcpyDeviceToHost, st));
+    LSP_CUDA(cudaStreamSynchronize(st));
+    // regulariser gradient (projector.cpp:34-54)
+    if (cfg.reg_beta != 0.0) {
+      if (cfg.reg_kind == LSP_REG_SQUARED) {
+        for (size_t i = 0; i < gp.size(); ++i) gp[i] += 2.0 * cfg.reg_beta * pv[i];
+        for (size_t i = 0; i < gq.size(); ++i) gq[i] += 2.0 * cfg.reg_beta * qv[i];
+      } else {
+        double pn = 0.0, qn = 0.0;
+        for (double x2 : pv) pn += x2 * x2;
+        for (double x2 : qv) qn += x2 * x2;
+        pn = std::sqrt(pn);
+        qn = std::sqrt(qn);
+        if (pn > 0.0)
+          for (size_t i = 0; i < gp.size(); ++i) gp[i] += cfg.reg_beta * pv[i] / pn;
+        if (qn > 0.0)
+          for (size_t i = 0; i < gq.size(); ++i) gq[i] += cfg.reg_beta * qv[i] / qn;
+      }
+    }
+  }
+};
+
+lsp_fit_config cfg_or_default(const lsp_fit_config* cfg) {
+  return cfg ? *cfg : lsp_fit_config_default();
+}
+
+template <typename F>
+int guard_fit(F&& f) {
+  try {
+    f();
+    return LSP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LSP_EINVAL;
+  }
+}
+
+}  // namespace
+}  // namespace lspb
+
+using namespace lspb;
+
+extern "C" {
+
+int lsp_fit_loss(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_dtype dtype,
+                 const lsp_fit_config* cfg, double* loss, lsp_stream_t stream) {
+  return guard_fit([&] {
+    require(pair && targets && loss, "fit_loss: null argument");
+    const lsp_fit_config c = cfg_or_default(cfg);
+    FitEngine fe(*pair, targets, t, ld, dtype, as_stream(stream));
+    fe.loss(pair->p->h_val, pair->q->h_val, c, loss, nullptr);
+  });
+}
+
+int lsp_fit_gradient(lsp_pair_t pair, const void* const* targets, int t, int64_t ld,
+                     lsp_dtype dtype, const lsp_fit_config* cfg, double* grad_p, double* grad_q,
+                     lsp_stream_t stream) {
+  return guard_fit([&] {
+    require(pair && targets && grad_p && grad_q, "fit_gradient: null argument");
+    const lsp_fit_config c = cfg_or_default(cfg);
+    FitEngine fe(*pair, targets, t, ld, dtype, as_stream(stream));
+    std::vector<double> gp, gq;
+    fe.gradient(pair->p->h_val, pair->q->h_val, c, gp, gq);
+    std::copy(gp.begin(), gp.end(), grad_p);
+    std::copy(gq.begin(), gq.end(), grad_q);
+  });
+}
+
+// fit: gradient descent on the values with a <=40-halving backtracking line
+// search, stopping on mean relative bias <= alpha (projector.cpp:253-315).
+int lsp_fit(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_dtype dtype,
+            const lsp_fit_config* cfg, lsp_fit_report* report, double* loss_curve, int max_curve,
+            lsp_stream_t stream) {
+  return guard_fit([&] {
+    require(pair && targets && report, "fit: null argument");
+    require(t >= 1, "fit: empty target corpus");
+    const lsp_fit_config c = cfg_or_default(cfg);
+    if (c.alpha <= 0.0 || c.alpha > 1.0) fail(LSP_EINVAL, "fit: alpha must be in (0, 1]");
+    if (c.max_steps < 1) fail(LSP_EINVAL, "fit: max_steps must be >= 1");
+    if (c.step_size <= 0.0) fail(LSP_EINVAL, "fit: step_size must be positive");
+    FitEngine fe(*pair, targets, t, ld, dtype, as_stream(stream));
+    std::vector<double> pv = pair->p->h_val, qv = pair->q->h_val;
+    const int budget = std::min(c.max_steps, c.timeout_steps);
+    *report = lsp_fit_report{};
+    int ncurve = 0;
+    auto push = [&](double l) {
+      if (loss_curve && ncurve < max_curve) loss_curve[ncurve] = l;
+      ++ncurve;
+    };
+    double loss = 0.0, rel = 0.0;
+    fe.loss(pv, qv, c, &loss, &rel);
+    if (!std::isfinite(loss)) fail(LSP_ENUMERIC, "fit: non-finite loss at initialization");
+    push(loss);
+    bool success = rel <= c.alpha, stalled = false;
+    std::vector<double> gp, gq, tp(pv.size()), tq(qv.size());
+    for (int step = 0; step < budget && !success; ++step) {
+      fe.gradient(pv, qv, c, gp, gq);
+      double trial_step = c.step_size;
+      bool accepted = false;
+      for (int halving = 0; halving < 40; ++halving) {
+        for (size_t i = 0; i < pv.size(); ++i) tp[i] = pv[i] - trial_step * gp[i];
+        for (size_t i = 0; i < qv.size(); ++i) tq[i] = qv[i] - trial_step * gq[i];
+        double tl = 0.0, trel = 0.0;
+        fe.loss(tp, tq, c, &tl, &trel);
+        if (std::isfinite(tl) && tl < loss) {
+          pv.swap(tp);
+          qv.swap(tq);
+          loss = tl;
+          rel = trel;
+          accepted = true;
+          break;
+        }
+        trial_step *= 0.5;
+      }
+      if (!accepted) {
+        stalled = true;
+        break;
+      }
+      ++report->steps;
+      push(loss);
+      success = rel <= c.alpha;
+    }
+    report->final_rel_bias = rel;
+    report->success = success ? 1 : 0;
+    report->stalled = stalled ? 1 : 0;
+    report->timed_out = (!success && !stalled) ? 1 : 0;
+    report->n_loss = ncurve;
+    // write the fitted values back (positions are frozen)
+    pair->p->h_val = pv;
+    pair->q->h_val = qv;
+    pair->p->upload_values();
+    pair->q->upload_values();
+  });
+}
+
+int lsp_projector_gram(lsp_projector_t a, lsp_projector_t b, double* out, lsp_stream_t stream) {
+  return guard_fit([&] {
+    require(a && b && out, "projector_gram: null argument");
+    if (a->n_rows != b->n_rows) fail(LSP_EINVAL, "projector_gram: row spaces differ");
+    cudaStream_t st = as_stream(stream);
+    LSP_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(a->d) * b->d * 8, st));
+    LSP_DISPATCH_ACC(a->compute, Ta, {
+      LSP_DISPATCH_ACC(b->compute, Tb, {
+        k_gram<Ta, Tb><<<ceil_div(a->d, 128), 128, 0, st>>>(
+            a->d, b->d, b->r, a->csc_ptr.as<int>(), a->csc_row.as<int>(), a->csc_val.as<Ta>(),
+            b->pos.as<int>(), b->val.as<Tb>(), out);
+      })
+    })
+    after_launch("gram");
+  });
+}
+
+int lsp_reproject_state(lsp_adam_t st, lsp_pair_t old_pair, lsp_pair_t new_pair,
+                        lsp_transfer_kind kind, lsp_stream_t stream) {
+  return guard_fit([&] {
+    require(st && old_pair && new_pair, "reproject_state: null argument");
+    if (old_pair->d != new_pair->d) fail(LSP_EINVAL, "reproject_state: subspace widths differ");
+    if (old_pair->m != new_pair->m || old_pair->n != new_pair->n)
+      fail(LSP_EINVAL, "reproject_state: weight dims differ");
+    if (st->rows != old_pair->d || st->cols != old_pair->d)
+      fail(LSP_EINVAL, "reproject_state: state dims do not match pair");
+    cudaStream_t s = as_stream(stream);
+    const int d = old_pair->d;
+    const size_t dd = static_cast<size_t>(d) * d;
+    DevBuf tp, tq, tp2, tq2, mm, vv, tmp;
+    for (DevBuf* b : {&tp, &tq, &tp2, &tq2, &mm, &vv, &tmp}) b->ensure(dd * 8);
+    int rc = lsp_projector_gram(static_cast<lsp_projector_t>(new_pair->p),
+                                static_cast<lsp_projector_t>(old_pair->p), tp.as<double>(), stream);
+    if (rc) fail(rc, g_last_error);
+    rc = lsp_projector_gram(static_cast<lsp_projector_t>(old_pair->q),
+                            static_cast<lsp_projector_t>(new_pair->q), tq.as<double>(), stream);
+    if (rc) fail(rc, g_last_error);
+    // moments -> fp64 row layout
+    auto to_row64 = [&](const DevBuf& src, DevBuf& dst) {
+      launch_convert(dd, src.p, st->compute, tmp.p, LSP_F64, s);
+      if (st->layout == LSP_LAYOUT_T)
+        launch_transpose(d, d, tmp.p, d, dst.p, d, LSP_F64, s);
+      else
+        LSP_CUDA(cudaMemcpyAsync(dst.p, tmp.p, dd * 8, cudaMemcpyDeviceToDevice, s));
+    };
+    auto from_row64 = [&](DevBuf& src, DevBuf& dst) {
+      const void* p = src.p;
+      if (st->layout == LSP_LAYOUT_T) {
+        launch_transpose(d, d, src.p, d, tmp.p, d, LSP_F64, s);
+        p = tmp.p;
+      }
+      launch_convert(dd, p, LSP_F64, dst.p, st->compute, s);
+    };
+    to_row64(st->m, mm);
+    to_row64(st->v, vv);
+    if (kind == LSP_TRANSFER_ENTRYWISE) {
+      LSP_CUDA(cudaMemcpyAsync(tp2.p, tp.p, dd * 8, cudaMemcpyDeviceToDevice, s));
+      LSP_CUDA(cudaMemcpyAsync(tq2.p, tq.p, dd * 8, cudaMemcpyDeviceToDevice, s));
+      k_square<<<egrid(dd), 256, 0, s>>>(dd, tp2.as<double>());
+      after_launch("square");
+      k_square<<<egrid(dd), 256, 0, s>>>(dd, tq2.as<double>());
+      after_launch("square");
+    } else {
+      dgemm(d, d, d, tp.as<double>(), tp.as<double>(), tp2.as<double>(), s);
+      dgemm(d, d, d, tq.as<double>(), tq.as<double>(), tq2.as<double>(), s);
+    }
+    DevBuf t1;
+    t1.ensure(dd * 8);
+    dgemm(d, d, d, tp.as<double>(), mm.as<double>(), t1.as<double>(), s);
+    dgemm(d, d, d, t1.as<double>(), tq.as<double>(), mm.as<double>(), s);
+    dgemm(d, d, d, tp2.as<double>(), vv.as<double>(), t1.as<double>(), s);
+    dgemm(d, d, d, t1.as<double>(), tq2.as<double>(), vv.as<double>(), s);
+    k_clamp0<<<egrid(dd), 256, 0, s>>>(dd, vv.as<double>());
+    after_launch("clamp0");
+    from_row64(mm, st->m);
+    from_row64(vv, st->v);
+    LSP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"
