@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""Benchmark of the LSP projector hot path (BASELINE.json metric):
+
+    grad GB/s (compress + decompress + apply) vs HBM peak; ms/step per layer stack
+
+A step = one pass of the hot path over one synthetic gradient per linear layer
+of the model: per matrix, compress S = P^T G Q, (all-reduce S over ranks),
+subspace Adam, fused decompress-and-apply W -= lr P dS Q^T, layers visited in
+backward order.  Inputs are resident in HBM (larger than L2: no flush needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank processes its own synthetic gradients (weak
+scaling, data parallel); the per-matrix S is all-reduced (mean) over NCCL and the
+update is replicated.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KINIT = 0x1A171  # proj/src/trainer.cpp:23 (projector init tag)
+
+# name -> (description, layers, [(m, n, count)], d (subspace), r (nnz/row), g dtype, w dtype)
+CONFIGS = {
+    "c1": ("single 1024x1024 weight, d=256, r=4 (BASELINE configs[0])", 1,
+           [(1024, 1024, 1)], 256, 4, "f32", "f32"),
+    "c2": ("GPT-2 774M 36-layer stack, d=512, r=4, fp32 (BASELINE configs[1])", 36,
+           [(1280, 1280, 4), (1280, 5120, 1), (5120, 1280, 1)], 512, 4, "f32", "f32"),
+    "c3": ("1.3B decoder 24-layer stack, d=1024, r=4, bf16 (BASELINE configs[2])", 24,
+           [(2048, 2048, 4), (2048, 5504, 2), (5504, 2048, 1)], 1024, 4, "bf16", "bf16"),
+    "c4": ("Llama-7B 32-layer stack, d=1024, r=4, fp32 (BASELINE configs[3])", 32,
+           [(4096, 4096, 4), (4096, 11008, 2), (11008, 4096, 1)], 1024, 4, "f32", "f32"),
+    "c4-bf16": ("Llama-7B 32-layer stack, d=1024, r=4, bf16 (BASELINE configs[3])", 32,
+                [(4096, 4096, 4), (4096, 11008, 2), (11008, 4096, 1)], 1024, 4, "bf16", "bf16"),
+}
+BYTES = {"f32": 4, "bf16": 2, "f64": 8}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c5"])
+    ap.add_argument("--d", type=int, default=None, help="c5 sweep: subspace width")
+    ap.add_argument("--r", type=int, default=None, help="c5 sweep: nonzeros per row")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def workload(args):
+    if args.config == "c5":
+        d, r = args.d or 1024, args.r or 4
+        return (f"4096x11008 d/r sweep, d={d}, r={r}, fp32 (BASELINE configs[4])", 1,
+                [(4096, 11008, 1)], d, r, "f32", "f32")
+    desc, L, shapes, d, r, gdt, wdt = CONFIGS[args.config]
+    if args.d:
+        d = args.d
+    if args.r:
+        r = args.r
+    return desc, L, shapes, d, r, gdt, wdt
+
+
+def matrices(L, shapes):
+    """Per-layer matrix list in the reference's (fan_in x fan_out) orientation."""
+    out = []
+    for layer in range(L):
+        for (m, n, cnt) in shapes:
+            for _ in range(cnt):
+                out.append((layer, m, n))
+    return out
+
+
+def b_alg(m, n, d, r, bg, bw, bv=4):
+    """algorithmic HBM bytes of one matrix step."""
+    return m * n * (bg + 2 * bw) + 24 * d * d + 2 * (m + n) * r * (4 + bv)
+
+
+def apply_bytes(m, n, d, r, bw, bv=4):
+    """Algorithmic bytes of one decompress-and-apply launch: W read+write once,
+    delta^T read once, CSR (pos, val) of P and Q read once."""
+    return 2 * m * n * bw + 4 * d * d + (m + n) * r * (4 + bv)
+
+
+def compress_bytes(m, n, d, r, bg, bv=4):
+    """Algorithmic bytes of one compress (stage 1 + 2): G read once, S written once,
+    projector entries read once."""
+    return m * n * bg + 4 * d * d + (m + n) * r * (4 + bv)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference (oracle/_ref) or the oracle port, on host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(desc, L, shapes, d, r, gdt, lr, reps=1, target_s=12.0):
+    import oracle
+
+    kind = "reference" if oracle.available("reference") else "port"
+    O = oracle.Oracle(kind)
+    cores = os.cpu_count() or 1
+    per_layer = sum(c for _, _, c in shapes)
+    layers = max(1, cores // per_layer)
+    rng = np.random.default_rng(0)
+    jobs = []
+    for (m, n, cnt) in shapes:
+        P = O.init_sparse(m, d, r, O.derive_seed(1, KINIT, 0))
+        Q = O.init_sparse(n, d, r, O.derive_seed(1, KINIT, 1))
+        g = rng.standard_normal((m, n)).astype(np.float32).astype(np.float64)
+        w = (0.02 * rng.standard_normal((m, n))).astype(np.float32).astype(np.float64)
+        jobs.append((P, Q, g, w, cnt * layers))
+    threads = sum(j[4] for j in jobs)
+    times = []
+    if kind != "reference":
+        # the port has no threaded timer: time one matrix per shape serially
+        t0 = time.perf_counter()
+        for P, Q, g, w, cnt in jobs:
+            s = O.compress(P, Q, g)
+            z = np.zeros_like(s)
+            _, _, de, _ = O.adam_step(z, z, s, 0)
+            O.decompress_apply(P, Q, de, lr, w)
+        t = time.perf_counter() - t0
+        gb = sum(P.n_rows * Q.n_rows for P, Q, *_ in jobs) * BYTES[gdt] / 1e9
+        return {"value": gb / t, "unit": "GB/s", "cores": 1, "kind": kind,
+                "sample": f"one matrix of each layer shape, serial, {t:.1f}s"}, t
+    for _ in range(reps):
+        res = [0.0] * len(jobs)
+
+        def run(i, job):
+            P, Q, g, w, cnt = job
+            res[i] = O.time_step(P, Q, g, w, lr, cnt, cnt)
+
+        th = [threading.Thread(target=run, args=(i, j)) for i, j in enumerate(jobs)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    gb = layers * sum(m * n * c for m, n, c in shapes) * BYTES[gdt] / 1e9
+    return {"value": gb / t, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": (f"{layers} layer(s) = {threads} matrices of the {desc.split(',')[0]} "
+                       f"shapes, one reference step each (compress, adam_step, "
+                       f"W -= decompress*lr) on {threads} std::threads, median of {reps}; "
+                       f"{t:.1f}s per sample")}, t
+
+
+def run_reference(args):
+    desc, L, shapes, d, r, gdt, wdt = workload(args)
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for _ in range(args.warmup + args.steps):
+        cb, t = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr)
+        samples.append(cb)
+    vals = [c["value"] for c in samples[args.warmup:]]
+    v = float(np.median(vals))
+    cb = dict(samples[-1])
+    cb["value"] = v
+    total_gb = L * sum(m * n * c for m, n, c in shapes) * BYTES[gdt] / 1e9
+    line = {"metric": "grad GB/s (compress+decompress+apply)", "value": v, "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total_gb / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "d": d, "r": r, "layers": L,
+                       "note": "ms_per_step extrapolated from the bounded sample to the full stack"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_10181_b200 as lsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    desc, L, shapes, d, r, gdt, wdt = workload(args)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
+    mats = matrices(L, shapes)
+
+    # ---- setup (not timed): one lsp.Layer (grouped launches) per model layer ----
+    items, layers = [], []
+    gen = torch.Generator(device=dev)
+    for layer_idx in range(L):
+        pairs = []
+        for idx, (lay, m, n) in enumerate(mats):
+            if lay != layer_idx:
+                continue
+            # projectors: the reference trainer seed path, identical on every rank
+            pp, pv = lsp.init_sparse(m, d, r, lsp.derive_seed(args.seed, KINIT, 2 * idx))
+            qp, qv = lsp.init_sparse(n, d, r, lsp.derive_seed(args.seed, KINIT, 2 * idx + 1))
+            pair = lsp.DevicePair(lsp.DeviceProjector(m, d, r, pp, pv),
+                                  lsp.DeviceProjector(n, d, r, qp, qv))
+            gen.manual_seed(lsp.derive_seed(args.seed, 0x6, idx * world + rank))
+            g = torch.randn(m, n, device=dev, generator=gen).to(tdt[gdt])
+            w = (0.02 * torch.randn(m, n, device=dev, generator=gen)).to(tdt[wdt])
+            items.append(dict(m=m, n=n, pair=pair, g=g, w=w))
+            pairs.append((pair, g, w))
+        lay = lsp.Layer([p for p, _, _ in pairs])
+        for i, (_, g, w) in enumerate(pairs):
+            lay.bind(i, g, w)
+        layers.append(lay)
+    torch.cuda.synchronize()
+    order = list(reversed(range(L)))  # backward order: last layer's gradients arrive first
+
+    stream = torch.cuda.current_stream()
+    ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(L)] for k in ("compress", "adam", "apply")}
+
+    def one_step(record=False):
+        """compress(l) -> all-reduce(S_l) -> adam(l) -> apply(l), one layer behind:
+        the all-reduce of layer l overlaps the compress of layer l-1."""
+        pending = None
+        for j, li in enumerate(order):
+            lay = layers[li]
+            if record:
+                ev["compress"][j][0].record(stream)
+            lay.compress()
+            if record:
+                ev["compress"][j][1].record(stream)
+            work = None
+            if world > 1:
+                work = dist.all_reduce(lay.s_buffer(), op=dist.ReduceOp.AVG, async_op=True)
+            if pending is not None:
+                finish(*pending, record)
+            pending = (j, li, work)
+        finish(*pending, record)
+
+    def finish(j, li, work, record):
+        lay = layers[li]
+        if work is not None:
+            work.wait()
+        if record:
+            ev["adam"][j][0].record(stream)
+        lay.adam(check_finite=world > 1)
+        if record:
+            ev["adam"][j][1].record(stream)
+            ev["apply"][j][0].record(stream)
+        lay.apply(args.lr)
+        if record:
+            ev["apply"][j][1].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # ---- timed region -------------------------------------------------------
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lsp.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.steps):
+        one_step(record=(k == args.steps - 1))
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lsp.launch_count() - launches0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    comp_ms = [a.elapsed_time(b) for a, b in ev["compress"]]
+    adam_ms = [a.elapsed_time(b) for a, b in ev["adam"]]
+    app_ms = [a.elapsed_time(b) for a, b in ev["apply"]]
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    for lay in layers:
+        lay.check()  # no non-finite gradients were seen
+
+    bg, bw = BYTES[gdt], BYTES[wdt]
+    grad_bytes = sum(it["m"] * it["n"] for it in items) * bg
+    value = world * grad_bytes / (ms * 1e-3) / 1e9
+    balg = sum(b_alg(it["m"], it["n"], d, r, bg, bw) for it in items)
+    peak, peak_src = measured_peaks()
+    # dominant kernel: the grouped decompress-and-apply (one k_decompress_band
+    # launch per layer, bracketed alone by the "apply" events)
+    app_bytes = sum(apply_bytes(it["m"], it["n"], d, r, bw) for it in items) / L
+    comp_bytes = sum(compress_bytes(it["m"], it["n"], d, r, bg) for it in items) / L
+    app_avg = float(np.mean(app_ms))
+    comp_avg = float(np.mean(comp_ms))
+    app_ach = app_bytes / (app_avg * 1e-3) / 1e9
+    comp_ach = comp_bytes / (comp_avg * 1e-3) / 1e9
+    tsum = sum(app_ms) + sum(comp_ms) + sum(adam_ms)
+    line = {
+        "metric": "grad GB/s (compress+decompress+apply)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (torch.randn gradients/weights in HBM; projectors from the reference "
+                "trainer seed path)",
+        "config": {"workload": desc, "matrices": len(items), "layers": L, "d": d, "r": r,
+                   "g_dtype": gdt, "w_dtype": wdt,
+                   "params": int(sum(it["m"] * it["n"] for it in items)),
+                   "l2": "inputs larger than L2 (%.1f GB of G per rank, streamed once)"
+                         % (grad_bytes / 1e9),
+                   "parallelism": f"dp{world}",
+                   "step_hbm_bytes_alg": balg,
+                   "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
+                   "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},
+        "roofline": {"kernel": "k_decompress_band (grouped fused decompress-and-apply, 1 launch "
+                               "per layer)",
+                     "bound": "hbm", "achieved": app_ach, "peak": peak, "unit": "GB/s",
+                     "frac": app_ach / peak, "traffic": None, "peak_source": peak_src,
+                     "bytes_per_launch_avg": app_bytes, "avg_launch_ms": app_avg,
+                     "share_of_step": sum(app_ms) / (ms if ms > 0 else 1)},
+        "breakdown": {"compress_ms_per_step": sum(comp_ms), "adam_ms_per_step": sum(adam_ms),
+                      "apply_ms_per_step": sum(app_ms), "other_ms_per_step": ms - tsum,
+                      "compress_achieved_gbs": comp_ach, "compress_frac": comp_ach / peak,
+                      "apply_achieved_gbs": app_ach},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, _ = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr)
+        line["cpu_baseline"] = cb
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, items, layers, order, world, dist, torch, dev, bg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(args, items, layers, order, world, dist, torch, dev, bg):
+    """Same metric through the C-ABI with HOST gradients: every step copies each
+    layer's G matrices from pinned host memory (copy stream, double-buffered per
+    layer) into the bound device buffers, runs the layer step, and reads the
+    layer's (all-reduced) S back to pinned host memory."""
+    per_layer = len(items) // len(layers)
+    host = {}
+    for it in items:
+        key = (it["m"], it["n"])
+        if key not in host:
+            h = torch.empty(it["m"], it["n"], dtype=it["g"].dtype, pin_memory=True)
+            h.copy_(torch.randn(it["m"], it["n"]).to(it["g"].dtype))
+            host[key] = h
+    s_host = [torch.empty(tuple(l.s_buffer().shape), dtype=l.s_buffer().dtype, pin_memory=True)
+              for l in layers]
+    main = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=dev)
+    steps = max(1, min(args.steps, 3))
+
+    def h2d(li):
+        with torch.cuda.stream(copy):
+            copy.wait_stream(main)  # the layer's G buffers are free (previous compress done)
+            for it in items[li * per_layer:(li + 1) * per_layer]:
+                it["g"].copy_(host[(it["m"], it["n"])], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(copy)
+        return e
+
+    def run_step():
+        nxt = h2d(order[0])
+        for j, li in enumerate(order):
+            e = nxt
+            if j + 1 < len(order):
+                nxt = h2d(order[j + 1])
+            main.wait_event(e)
+            lay = layers[li]
+            lay.compress()
+            if world > 1:
+                dist.all_reduce(lay.s_buffer(), op=dist.ReduceOp.AVG)
+            lay.update(args.lr, check_finite=world > 1)
+            s_host[li].copy_(lay.s_buffer(), non_blocking=True)
+        torch.cuda.synchronize()
+
+    run_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run_step()
+    if world > 1:
+        dist.barrier()
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        tt = torch.tensor([dt], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    gbytes = sum(it["m"] * it["n"] for it in items) * bg
+    return {"value": world * gbytes / dt / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": int(gbytes),
+            "d2h_bytes_per_step": int(sum(l.s_buffer().numel() * 4 for l in layers)),
+            "ms_per_step": dt * 1e3, "steps": steps,
+            "note": "wall clock incl. H2D of every G from pinned host memory and D2H of every S"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,7 @@ typedef enum { LSP_TRANSFER_ENTRYWISE = 0, LSP_TRANSFER_MATRIX = 1 } lsp_transfe
 typedef struct lsp_projector_s* lsp_projector_t; /* device SparseProjector (CSR + CSC) */
 typedef struct lsp_pair_s* lsp_pair_t;           /* ProjectorPair + device workspace   */
 typedef struct lsp_adam_s* lsp_adam_t;           /* device SubspaceOptState            */
+typedef struct lsp_layer_s* lsp_layer_t;         /* per-layer schedule unit            */
 typedef void* lsp_stream_t;                      /* cudaStream_t (NULL = legacy stream) */
 
 /* proj/include/lsp/projector.hpp:43-51 */
@@ -142,6 +143,18 @@ int lsp_projector_destroy(lsp_projector_t p);
 int lsp_pair_create(lsp_projector_t p, lsp_projector_t q, lsp_pair_t* out);
 int lsp_pair_destroy(lsp_pair_t pair);
 
+/* Generic sparse products with one projector P (n_rows x d when densified),
+ * proj/src/projector.cpp:105-161.  x and out are device matrices in the
+ * projector's compute dtype:
+ *   LSP_LEFT     out (n_rows x cols) = P   x (d x cols)        left_mul
+ *   LSP_LEFT_T   out (d x cols)      = P^T x (n_rows x cols)   leftT_mul
+ *   LSP_RIGHT    out (rows x d)      = x (rows x n_rows) P     right_mul
+ *   LSP_RIGHT_T  out (rows x n_rows) = x (rows x d) P^T        rightT_mul
+ * `rows`/`cols` give the free dimension of x (cols for LEFT*, rows for RIGHT*). */
+typedef enum { LSP_LEFT = 0, LSP_LEFT_T = 1, LSP_RIGHT = 2, LSP_RIGHT_T = 3 } lsp_mul_op;
+int lsp_projector_mul(lsp_projector_t p, int op, int free_dim, const void* x, int64_t ldx,
+                      void* out, int64_t ldo, lsp_stream_t stream);
+
 /* ----------------------------------------------------------------------------
  * Hot path (device pointers, asynchronous on `stream`)
  * -------------------------------------------------------------------------- */
@@ -205,6 +218,41 @@ int lsp_step(lsp_pair_t pair, lsp_adam_t st, const void* g, int64_t ldg, lsp_dty
  * lsp_update to run Adam and the decompress-and-apply. */
 int lsp_update(lsp_pair_t pair, lsp_adam_t st, const void* s_t, void* w, int64_t ldw,
                lsp_dtype w_dtype, double lr, lsp_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Per-layer schedule (the body of proj/src/trainer.cpp:186-198 for every
+ * linear layer of a block): up to 16 pairs sharing d, r and the compute dtype,
+ * stepped with ONE grouped launch per stage.  The layer owns contiguous
+ * S^T / delta^T buffers and the Adam moments of all its matrices (beta/eps as
+ * make_opt_state), so a data-parallel caller all-reduces a whole layer's S
+ * with a single collective between lsp_layer_compress and lsp_layer_update.
+ * -------------------------------------------------------------------------- */
+int lsp_layer_create(int count, const lsp_pair_t* pairs, double beta1, double beta2, double eps,
+                     lsp_layer_t* out);
+int lsp_layer_destroy(lsp_layer_t layer);
+/* Bind matrix idx's gradient G (m x n) and weight W (m x n); all matrices of a
+ * layer must share the G dtype and the W dtype. */
+int lsp_layer_bind(lsp_layer_t layer, int idx, const void* g, int64_t ldg, lsp_dtype g_dtype,
+                   void* w, int64_t ldw, lsp_dtype w_dtype);
+/* Device pointer to the layer's contiguous S^T buffer (count blocks of d x d,
+ * compute dtype) and its element count. */
+int lsp_layer_s_buffer(lsp_layer_t layer, void** s_t, int64_t* count);
+/* S^T_i = (P_i^T G_i Q_i)^T for every matrix (latches the non-finite flag). */
+int lsp_layer_compress(lsp_layer_t layer, lsp_stream_t stream);
+/* Adam on the layer's S^T (optionally re-checking finiteness, e.g. after an
+ * all-reduce) and W_i -= lr * P_i delta_i Q_i^T; skipped if the flag is set. */
+int lsp_layer_update(lsp_layer_t layer, double lr, int check_finite, lsp_stream_t stream);
+/* The two halves of lsp_layer_update: Adam -> delta^T, then the fused
+ * decompress-and-apply of every matrix (one grouped launch each). */
+int lsp_layer_adam(lsp_layer_t layer, int check_finite, lsp_stream_t stream);
+int lsp_layer_apply(lsp_layer_t layer, double lr, lsp_stream_t stream);
+/* compress + update. */
+int lsp_layer_step(lsp_layer_t layer, double lr, lsp_stream_t stream);
+/* SYNCHRONOUS: LSP_ENUMERIC if a non-finite S was seen (clears the flag). */
+int lsp_layer_check(lsp_layer_t layer, lsp_stream_t stream);
+/* SYNCHRONOUS host copy of matrix idx's moments and the shared step. */
+int lsp_layer_adam_get(lsp_layer_t layer, int idx, double* m, double* v, int64_t* step,
+                       lsp_layout layout);
 
 /* ----------------------------------------------------------------------------
  * Projector fit (proj/src/projector.cpp:189-315), on the device in fp64.

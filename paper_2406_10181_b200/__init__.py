@@ -30,6 +30,7 @@ from .projector import (  # noqa: F401
     DeviceProjector,
     FitConfig,
     FitReport,
+    Layer,
     derive_seed,
     identity_pattern,
     init_sparse,
@@ -43,7 +44,7 @@ from .projector import (  # noqa: F401
 )
 
 __all__ = [
-    "AdamState", "DevicePair", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
+    "AdamState", "DevicePair", "Layer", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
     "identity_pattern", "init_sparse", "load_projector", "projector_gram", "reproject_state",
     "save_projector", "step", "subsample_size", "update", "LspError", "InvalidArgument",
     "NumericError", "IoError", "CudaError", "Layout", "lib", "library_path", "launch_count",

@@ -89,6 +89,7 @@ _SIGS = {
     "lsp_projector_get": (_i, [_vp, _i32p, _dp]),
     "lsp_projector_shape": (_i, [_vp, _ip, _ip, _ip]),
     "lsp_projector_destroy": (_i, [_vp]),
+    "lsp_projector_mul": (_i, [_vp, _i, _i, _vp, _i64, _vp, _i64, _vp]),
     "lsp_pair_create": (_i, [_vp, _vp, C.POINTER(_vp)]),
     "lsp_pair_destroy": (_i, [_vp]),
     "lsp_compress": (_i, [_vp, _vp, _i64, _i, _vp, _i, _vp]),
@@ -105,6 +106,17 @@ _SIGS = {
     "lsp_adam_info": (_i, [_vp, _ip, _ip, _dp, _dp, _dp]),
     "lsp_step": (_i, [_vp, _vp, _vp, _i64, _i, _vp, _i64, _i, _d, _vp, _vp]),
     "lsp_update": (_i, [_vp, _vp, _vp, _vp, _i64, _i, _d, _vp]),
+    "lsp_layer_create": (_i, [_i, C.POINTER(_vp), _d, _d, _d, C.POINTER(_vp)]),
+    "lsp_layer_destroy": (_i, [_vp]),
+    "lsp_layer_bind": (_i, [_vp, _i, _vp, _i64, _i, _vp, _i64, _i]),
+    "lsp_layer_s_buffer": (_i, [_vp, C.POINTER(_vp), C.POINTER(_i64)]),
+    "lsp_layer_compress": (_i, [_vp, _vp]),
+    "lsp_layer_update": (_i, [_vp, _d, _i, _vp]),
+    "lsp_layer_adam": (_i, [_vp, _i, _vp]),
+    "lsp_layer_apply": (_i, [_vp, _d, _vp]),
+    "lsp_layer_step": (_i, [_vp, _d, _vp]),
+    "lsp_layer_check": (_i, [_vp, _vp]),
+    "lsp_layer_adam_get": (_i, [_vp, _i, _dp, _dp, C.POINTER(_i64), _i]),
     "lsp_fit_loss": (_i, [_vp, C.POINTER(_vp), _i, _i64, _i, C.POINTER(FitConfigC), _dp, _vp]),
     "lsp_fit_gradient": (_i, [_vp, C.POINTER(_vp), _i, _i64, _i, C.POINTER(FitConfigC), _dp,
                               _dp, _vp]),
@@ -129,7 +141,7 @@ class _Lib:
                 raise ImportError(
                     f"{library_path} is not built; run `python -c \"import __graft_entry__ as g; "
                     "g.build()\"` (nvcc, sm_100a)")
-            cdll = C.CDLL(library_path, mode=C.RTLD_GLOBAL)
+            cdll = C.CDLL(library_path, mode=C.RTLD_LOCAL)
             for name, (res, args) in _SIGS.items():
                 fn = getattr(cdll, name)
                 fn.restype = res

@@ -145,6 +145,10 @@ double sumsq_sync(Pair& pr, int rows, int cols, const void* x, long long ld, lsp
 
 using namespace lspb;
 
+static void check_ld(long long ld, int cols, const char* what) {
+  if (ld < cols) fail(LSP_EINVAL, std::string(what) + ": leading dimension smaller than columns");
+}
+
 template <typename T>
 static void moments_to_host(const Adam& a, const DevBuf& b, double* out, lsp_layout layout) {
   std::vector<T> tmp(a.count());
@@ -317,10 +321,60 @@ int lsp_pair_destroy(lsp_pair_t pair) {
   return guard([&] { delete pair; });
 }
 
-// ---- hot path ------------------------------------------------------------------
-static void check_ld(long long ld, int cols, const char* what) {
-  if (ld < cols) fail(LSP_EINVAL, std::string(what) + ": leading dimension smaller than columns");
+int lsp_projector_mul(lsp_projector_t p, int op, int free_dim, const void* x, int64_t ldx,
+                      void* out, int64_t ldo, lsp_stream_t stream) {
+  return guard([&] {
+    require(p && x && out, "projector_mul: null argument");
+    require(free_dim >= 0, "projector_mul: negative dimension");
+    cudaStream_t st = as_stream(stream);
+    const Projector& P = *p;
+    const lsp_dtype dt = P.compute;
+    const size_t vs = dtype_size(dt);
+    if (free_dim == 0) return;
+    switch (op) {
+      case LSP_LEFT:  // rows of x gathered by the CSR of P
+        check_ld(ldx, free_dim, "left_mul");
+        check_ld(ldo, free_dim, "left_mul");
+        launch_gather(P.n_rows, free_dim, nullptr, P.r, P.pos.as<int>(), P.val.p, dt, x, ldx,
+                      dt, nullptr, 0, out, ldo, dt, 1.0, 0.0, nullptr, nullptr, st);
+        break;
+      case LSP_LEFT_T:  // rows of x gathered by the CSC of P
+        check_ld(ldx, free_dim, "leftT_mul");
+        check_ld(ldo, free_dim, "leftT_mul");
+        launch_gather(P.d, free_dim, P.csc_ptr.as<int>(), 0, P.csc_row.as<int>(), P.csc_val.p,
+                      dt, x, ldx, dt, nullptr, 0, out, ldo, dt, 1.0, 0.0, nullptr, nullptr, st);
+        break;
+      case LSP_RIGHT:
+      case LSP_RIGHT_T: {
+        // x P = (P^T x^T)^T ;  x P^T = (P x^T)^T
+        const bool right = op == LSP_RIGHT;
+        const int in_cols = right ? P.n_rows : P.d;
+        const int out_cols = right ? P.d : P.n_rows;
+        check_ld(ldx, in_cols, "right_mul");
+        check_ld(ldo, out_cols, "right_mul");
+        DevBuf xt, yt;
+        xt.ensure(static_cast<size_t>(in_cols) * free_dim * vs);
+        yt.ensure(static_cast<size_t>(out_cols) * free_dim * vs);
+        launch_transpose(free_dim, in_cols, x, ldx, xt.p, free_dim, dt, st);
+        if (right)
+          launch_gather(P.d, free_dim, P.csc_ptr.as<int>(), 0, P.csc_row.as<int>(), P.csc_val.p,
+                        dt, xt.p, free_dim, dt, nullptr, 0, yt.p, free_dim, dt, 1.0, 0.0,
+                        nullptr, nullptr, st);
+        else
+          launch_gather(P.n_rows, free_dim, nullptr, P.r, P.pos.as<int>(), P.val.p, dt, xt.p,
+                        free_dim, dt, nullptr, 0, yt.p, free_dim, dt, 1.0, 0.0, nullptr, nullptr,
+                        st);
+        launch_transpose(out_cols, free_dim, yt.p, free_dim, out, ldo, dt, st);
+        LSP_CUDA(cudaStreamSynchronize(st));  // temporaries die here
+        break;
+      }
+      default:
+        fail(LSP_EINVAL, "projector_mul: unknown op");
+    }
+  });
 }
+
+// ---- hot path ------------------------------------------------------------------
 
 int lsp_compress(lsp_pair_t pair, const void* g, int64_t ldg, lsp_dtype g_dtype, void* s,
                  lsp_layout s_layout, lsp_stream_t stream) {
@@ -417,7 +471,8 @@ int lsp_adam_create(int rows, int cols, double beta1, double beta2, double eps,
       a->v.ensure(bytes);
       a->flag.ensure(sizeof(int));
       a->dstep.ensure(sizeof(long long));
-      a->corr.ensure(2 * sizeof(double));
+      a->done.ensure(sizeof(unsigned));
+      LSP_CUDA(cudaMemset(a->done.p, 0, sizeof(unsigned)));
       LSP_CUDA(cudaMemset(a->m.p, 0, bytes));
       LSP_CUDA(cudaMemset(a->v.p, 0, bytes));
       LSP_CUDA(cudaMemset(a->flag.p, 0, sizeof(int)));
@@ -511,10 +566,10 @@ static void check_step_args(lsp_pair_t pair, lsp_adam_t a) {
 }
 
 static void update_impl(Pair& pr, Adam& a, const void* s_t, void* w, long long ldw,
-                        lsp_dtype w_dtype, double lr, cudaStream_t st) {
+                        lsp_dtype w_dtype, double lr, cudaStream_t st, bool check) {
   pr.d_t.ensure(static_cast<size_t>(pr.d) * pr.d * dtype_size(pr.compute));
   // non-finite S -> skip Adam and the apply (NumericError semantics)
-  launch_check_finite(a.count(), s_t, a.compute, a.flag.as<int>(), st);
+  if (check) launch_check_finite(a.count(), s_t, a.compute, a.flag.as<int>(), st);
   launch_adam(a, s_t, pr.d_t.p, a.flag.as<int>(), st);
   launch_decompress(pr, pr.d_t.p, w, ldw, w, ldw, w_dtype, -lr, 1.0, a.flag.as<int>(), nullptr,
                     nullptr, st);
@@ -534,8 +589,9 @@ int lsp_step(lsp_pair_t pair, lsp_adam_t a, const void* g, int64_t ldg, lsp_dtyp
       pair->s_t.ensure(static_cast<size_t>(pair->d) * pair->d * dtype_size(pair->compute));
       s_t = pair->s_t.p;
     }
-    compress_T(*pair, g, ldg, g_dtype, s_t, st);
-    update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, st);
+    // stage 2 latches the non-finite flag while writing S, so no extra check pass
+    compress_T(*pair, g, ldg, g_dtype, s_t, st, a->flag.as<int>());
+    update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, st, false);
   });
 }
 
@@ -545,7 +601,7 @@ int lsp_update(lsp_pair_t pair, lsp_adam_t a, const void* s_t, void* w, int64_t 
     check_step_args(pair, a);
     require(s_t && w, "update: null argument");
     check_ld(ldw, pair->n, "update");
-    update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, as_stream(stream));
+    update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, as_stream(stream), true);
   });
 }
 

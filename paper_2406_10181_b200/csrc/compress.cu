@@ -59,48 +59,75 @@ __device__ __forceinline__ void load_tile(Tin* tile, const Tin* __restrict__ g, 
   }
 }
 
+// One stage-1 job (matrix) of a grouped launch.
+struct S1Mat {
+  const void* g;
+  long long ldg;
+  int m, n;
+  const int* split;
+  const void* ent;
+  int nchunks;
+  void* zt;
+  int ldz;
+  int band_end;  // exclusive prefix of bands over the group
+  int vec;
+};
+struct S1Args {
+  S1Mat mat[kMaxGroup];
+  int count;
+  int d;
+};
+
+// One CTA = one band of 32 columns of one matrix x (WARPS*32) bins.
 template <typename Tin, typename Tacc, int WARPS, int BM>
-__global__ void __launch_bounds__(WARPS * 32, 1)
-    k_compress_stage1(const Tin* __restrict__ g, long long ldg, int m, int n, int d,
-                      const int* __restrict__ split,
-                      const typename EntryOf<Tacc>::type* __restrict__ ent, int nchunks,
-                      Tacc* __restrict__ zt, int ldz, int vec) {
+__global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_constant__ S1Args A) {
+  using Ent = typename EntryOf<Tacc>::type;
   constexpr int NT = WARPS * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tin* tiles = reinterpret_cast<Tin*>(smem_raw);  // [2][BM][32]
+  // which matrix / band (uniform scan over <= kMaxGroup entries)
+  int mi = 0;
+  while (mi + 1 < A.count && static_cast<int>(blockIdx.x) >= A.mat[mi].band_end) ++mi;
+  const S1Mat& M = A.mat[mi];
+  const int band = blockIdx.x - (mi ? A.mat[mi - 1].band_end : 0);
+  const Tin* __restrict__ g = static_cast<const Tin*>(M.g);
+  const Ent* __restrict__ ent = static_cast<const Ent*>(M.ent);
+  const int* __restrict__ split = M.split;
+  const int d = A.d, m = M.m, n = M.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int j0 = blockIdx.x * 32;
+  const int j0 = band * 32;
   const int bin0 = blockIdx.y * NT + warp * 32;
   const int my_bin = bin0 + lane;
-  const bool vec16 = vec != 0;
+  const bool vec16 = M.vec != 0;
 
   Tacc acc[32];
 #pragma unroll
   for (int b = 0; b < 32; ++b) acc[b] = Tacc(0);
 
-  load_tile<Tin, BM, NT>(tiles, g, ldg, m, n, 0, j0, vec16);
+  load_tile<Tin, BM, NT>(tiles, g, M.ldg, m, n, 0, j0, vec16);
   cp_async_commit();
-  for (int c = 0; c < nchunks; ++c) {
+  for (int c = 0; c < M.nchunks; ++c) {
     // Chunk c+1 goes to the other buffer; the barrier below the wait also
     // guarantees every warp has finished reading it (chunk c-1).
     cp_async_wait<0>();
     __syncthreads();
-    if (c + 1 < nchunks)
-      load_tile<Tin, BM, NT>(tiles + ((c + 1) & 1) * BM * 32, g, ldg, m, n, (c + 1) * BM, j0,
+    if (c + 1 < M.nchunks)
+      load_tile<Tin, BM, NT>(tiles + ((c + 1) & 1) * BM * 32, g, M.ldg, m, n, (c + 1) * BM, j0,
                              vec16);
     cp_async_commit();
     const Tin* t = tiles + (c & 1) * BM * 32 + lane;
     // Entries of (chunk c, bin) are contiguous and bins follow each other, so
     // bin b's range is [end(b-1), end(b)).
     const long long base = static_cast<long long>(c) * d;
-    int e = split[base + min(bin0, d)];
-    const int my_end = split[base + min(my_bin + 1, d)];
+    int e = __ldg(split + base + min(bin0, d));
+    const int my_end = __ldg(split + base + min(my_bin + 1, d));
 #pragma unroll
     for (int b = 0; b < 32; ++b) {
       const int end = __shfl_sync(0xffffffffu, my_end, b);
       Tacc a = acc[b];
+#pragma unroll 1
       for (; e < end; ++e) {
-        const auto en = ent[e];
+        const Ent en = ent[e];
         a = fma(en.val, cvt<Tacc>(t[en.off]), a);
       }
       acc[b] = a;
@@ -108,8 +135,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
   const int j = j0 + lane;
   if (j < n) {
-    Tacc* dst = zt + static_cast<long long>(j) * ldz + bin0;
-    if (bin0 + 32 <= ldz && (ldz % 4) == 0 && sizeof(Tacc) == 4) {
+    Tacc* dst = static_cast<Tacc*>(M.zt) + static_cast<long long>(j) * M.ldz + bin0;
+    if (bin0 + 32 <= M.ldz && (M.ldz % 4) == 0 && sizeof(Tacc) == 4) {
 #pragma unroll
       for (int b = 0; b < 32; b += 4)
         *reinterpret_cast<float4*>(dst + b) =
@@ -117,51 +144,72 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     } else {
 #pragma unroll
       for (int b = 0; b < 32; ++b)
-        if (bin0 + b < ldz) dst[b] = acc[b];
+        if (bin0 + b < M.ldz) dst[b] = acc[b];
     }
   }
 }
 
 template <typename Tin, typename Tacc, int WARPS>
-void stage1_impl(const Pair& pr, const Tin* g, long long ldg, Tacc* zt, cudaStream_t st) {
-  constexpr int kStageBytes = WARPS >= 16 ? 65536 : 32768;
+void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
+  constexpr int kStageBytes = WARPS >= 16 ? (sizeof(Tin) == 4 ? 98304 : 65536) : 32768;
   constexpr int BM = kStageBytes / (32 * sizeof(Tin));
-  Projector& P = *pr.p;
-  const ChunkTable& ct = P.chunk_table(BM);
-  const int bins_per_cta = WARPS * 32;
-  dim3 grid(ceil_div(pr.n, 32), ceil_div(pr.d, bins_per_cta));
+  S1Args A{};
+  A.count = static_cast<int>(jobs.size());
+  A.d = d;
+  int bands = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const S1Job& J = jobs[i];
+    const ChunkTable& ct = J.pr->p->chunk_table(BM);
+    S1Mat& M = A.mat[i];
+    M.g = J.g, M.ldg = J.ldg, M.m = J.pr->m, M.n = J.pr->n;
+    M.split = ct.split.as<int>(), M.ent = ct.ent.p, M.nchunks = ct.nchunks;
+    M.zt = J.zt, M.ldz = J.pr->ldz();
+    bands += ceil_div(M.n, 32);
+    M.band_end = bands;
+    M.vec = (reinterpret_cast<uintptr_t>(J.g) % 16 == 0) &&
+            ((J.ldg * static_cast<long long>(sizeof(Tin))) % 16 == 0);
+  }
+  if (bands == 0) return;
+  dim3 grid(bands, ceil_div(d, WARPS * 32));
   const int smem = 2 * BM * 32 * sizeof(Tin);
   auto kern = k_compress_stage1<Tin, Tacc, WARPS, BM>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const bool vec = (reinterpret_cast<uintptr_t>(g) % 16 == 0) && ((ldg * sizeof(Tin)) % 16 == 0);
-  kern<<<grid, WARPS * 32, smem, st>>>(g, ldg, pr.m, pr.n, pr.d, ct.split.as<int>(),
-                                        ct.ent.as<typename EntryOf<Tacc>::type>(), ct.nchunks,
-                                        zt, pr.ldz(), vec ? 1 : 0);
+  kern<<<grid, WARPS * 32, smem, st>>>(A);
   after_launch("compress_stage1");
 }
 
 }  // namespace
 
-void launch_compress_stage1(const Pair& pr, const void* g, long long ldg, lsp_dtype gdt,
-                            void* zt, cudaStream_t st) {
-  LSP_DISPATCH_ACC(pr.compute, Tacc, {
+// Z^T_i = G_i^T P_i for every job of a group (same d, compute and G dtype).
+void launch_compress_stage1_group(const std::vector<S1Job>& jobs, lsp_dtype gdt,
+                                  cudaStream_t st) {
+  if (jobs.empty()) return;
+  require(jobs.size() <= static_cast<size_t>(kMaxGroup), "group too large");
+  const Pair& p0 = *jobs[0].pr;
+  LSP_DISPATCH_ACC(p0.compute, Tacc, {
     LSP_DISPATCH_STORAGE(gdt, Tin, {
-      const int need = ceil_div(pr.d, 32);  // warps needed to cover every bin once
+      const int need = ceil_div(p0.d, 32);  // warps needed to cover every bin once
       constexpr int kMaxWarps = sizeof(Tacc) == 8 ? 16 : 32;
       if constexpr (kMaxWarps == 32) {
         if (need > 16) {
-          stage1_impl<Tin, Tacc, 32>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+          stage1_impl<Tin, Tacc, 32>(jobs, p0.d, st);
           break;
         }
       }
       if (need > 8)
-        stage1_impl<Tin, Tacc, 16>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+        stage1_impl<Tin, Tacc, 16>(jobs, p0.d, st);
       else if (need > 4)
-        stage1_impl<Tin, Tacc, 8>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+        stage1_impl<Tin, Tacc, 8>(jobs, p0.d, st);
       else
-        stage1_impl<Tin, Tacc, 4>(pr, static_cast<const Tin*>(g), ldg, static_cast<Tacc*>(zt), st);
+        stage1_impl<Tin, Tacc, 4>(jobs, p0.d, st);
     })
   })
+}
+
+void launch_compress_stage1(const Pair& pr, const void* g, long long ldg, lsp_dtype gdt,
+                            void* zt, cudaStream_t st) {
+  std::vector<S1Job> jobs{S1Job{&pr, g, ldg, zt}};
+  launch_compress_stage1_group(jobs, gdt, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -284,16 +332,117 @@ void launch_transpose(int rows, int cols, const void* src, long long lds, void* 
   after_launch("transpose");
 }
 
-// S^T = Q^T (G^T P): stage 1 into pr.zt, stage 2 gather into s_t (d x d, ld d).
+// ---------------------------------------------------------------------------
+// Stage 2 (grouped, fp32): S^T_i[b][:] = sum_{t in CSC(Q_i)[b]} q_t Z^T_i[j_t][:].
+// One CTA per (subspace row b, matrix); a thread owns 4 consecutive columns;
+// four entries' rows are in flight per thread (L2-bound gathers of 4 KB rows).
+// Non-finite results latch `flag` (reference NumericError, subspace_opt.cpp:38).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct S2Mat {
+  const int* ptr;
+  const int* row;
+  const float* val;
+  const float* zt;
+  int ldz;
+  float* s_t;
+};
+struct S2Args {
+  S2Mat mat[kMaxGroup];
+  int count;
+  int d;
+  int* flag;
+};
+
+constexpr int kS2Threads = 256;
+
+__global__ void __launch_bounds__(kS2Threads) k_stage2_f4(const __grid_constant__ S2Args A) {
+  const S2Mat& M = A.mat[blockIdx.y];
+  const int b = blockIdx.x, d = A.d;
+  const int e0 = __ldg(M.ptr + b), e1 = __ldg(M.ptr + b + 1);
+  bool bad = false;
+  for (int a0 = 4 * threadIdx.x; a0 < d; a0 += 4 * kS2Threads) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      float4 z[4];
+      float q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        q[u] = __ldg(M.val + e + u);
+        z[u] = __ldg(reinterpret_cast<const float4*>(M.zt + static_cast<long long>(__ldg(M.row + e + u)) * M.ldz + a0));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x = fmaf(q[u], z[u].x, acc.x);
+        acc.y = fmaf(q[u], z[u].y, acc.y);
+        acc.z = fmaf(q[u], z[u].z, acc.z);
+        acc.w = fmaf(q[u], z[u].w, acc.w);
+      }
+    }
+    for (; e < e1; ++e) {
+      const float q = __ldg(M.val + e);
+      const float4 z = __ldg(reinterpret_cast<const float4*>(M.zt + static_cast<long long>(__ldg(M.row + e)) * M.ldz + a0));
+      acc.x = fmaf(q, z.x, acc.x);
+      acc.y = fmaf(q, z.y, acc.y);
+      acc.z = fmaf(q, z.z, acc.z);
+      acc.w = fmaf(q, z.w, acc.w);
+    }
+    bad |= !(isfinite(acc.x) && isfinite(acc.y) && isfinite(acc.z) && isfinite(acc.w));
+    *reinterpret_cast<float4*>(M.s_t + static_cast<long long>(b) * d + a0) = acc;
+  }
+  if (A.flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(A.flag, 1);
+}
+
+}  // namespace
+
+void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t st) {
+  if (jobs.empty()) return;
+  const Pair& p0 = *jobs[0].pr;
+  const int d = p0.d;
+  bool fast = p0.compute == LSP_F32 && d % 4 == 0;
+  for (const S1Job& J : jobs)
+    fast = fast && J.pr->ldz() % 4 == 0 && reinterpret_cast<uintptr_t>(J.zt) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(J.s_t) % 16 == 0;
+  if (fast) {
+    S2Args A{};
+    A.count = static_cast<int>(jobs.size());
+    A.d = d;
+    A.flag = flag;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+      const Projector& Q = *jobs[i].pr->q;
+      A.mat[i] = S2Mat{Q.csc_ptr.as<int>(), Q.csc_row.as<int>(), Q.csc_val.as<float>(),
+                       static_cast<const float*>(jobs[i].zt), jobs[i].pr->ldz(),
+                       static_cast<float*>(jobs[i].s_t)};
+    }
+    k_stage2_f4<<<dim3(d, A.count), kS2Threads, 0, st>>>(A);
+    after_launch("stage2");
+    return;
+  }
+  for (const S1Job& J : jobs) {
+    const Projector& Q = *J.pr->q;
+    launch_gather(d, d, Q.csc_ptr.as<int>(), 0, Q.csc_row.as<int>(), Q.csc_val.p, p0.compute,
+                  J.zt, J.pr->ldz(), p0.compute, nullptr, 0, J.s_t, d, p0.compute, 1.0, 0.0,
+                  nullptr, nullptr, st);
+    if (flag) launch_check_finite(static_cast<size_t>(d) * d, J.s_t, p0.compute, flag, st);
+  }
+}
+
+// S^T = Q^T (G^T P) for every job: grouped stage 1 into each job's zt, grouped stage 2.
+void compress_group_T(const std::vector<S1Job>& jobs, lsp_dtype gdt, int* flag,
+                      cudaStream_t st) {
+  launch_compress_stage1_group(jobs, gdt, st);
+  launch_stage2_group(jobs, flag, st);
+}
+
+// S^T = Q^T (G^T P) for one pair: stage 1 into pr.zt, stage 2 into s_t (d x d, ld d).
 void compress_T(Pair& pr, const void* g, long long ldg, lsp_dtype gdt, void* s_t,
-                cudaStream_t st) {
+                cudaStream_t st, int* flag) {
   const size_t vs = dtype_size(pr.compute);
   pr.zt.ensure(static_cast<size_t>(pr.n) * pr.ldz() * vs);
-  launch_compress_stage1(pr, g, ldg, gdt, pr.zt.p, st);
-  const Projector& Q = *pr.q;
-  launch_gather(pr.d, pr.d, Q.csc_ptr.as<int>(), 0, Q.csc_row.as<int>(), Q.csc_val.p,
-                pr.compute, pr.zt.p, pr.ldz(), pr.compute, nullptr, 0, s_t, pr.d, pr.compute,
-                1.0, 0.0, nullptr, nullptr, st);
+  std::vector<S1Job> jobs{S1Job{&pr, g, ldg, pr.zt.p, s_t}};
+  compress_group_T(jobs, gdt, flag, st);
 }
 
 }  // namespace lspb

@@ -106,14 +106,40 @@ struct Adam {
   DevBuf m, v;
   DevBuf flag;   // int: latched non-finite gradient
   DevBuf dstep;  // int64: step counter, advanced on the device (graph-replay safe)
-  DevBuf corr;   // double[2]: bias corrections (1-b1^t, 1-b2^t) of the current step
+  DevBuf done;   // unsigned: blocks finished in the current Adam launch
   size_t count() const { return static_cast<size_t>(rows) * cols; }
+};
+
+constexpr int kMaxGroup = 16;  // matrices per grouped launch (one layer)
+
+// One matrix of a grouped compress.
+struct S1Job {
+  const Pair* pr;
+  const void* g;
+  long long ldg;
+  void* zt;   // n x ldz workspace (compute dtype)
+  void* s_t;  // d x d output S^T (compute dtype)
+};
+
+// One matrix of a grouped decompress: out = beta*in + alpha * P delta Q^T.
+struct DecJob {
+  const Pair* pr;
+  const void* delta_t;  // d x d, ld d
+  const void* in;
+  long long ldi;
+  void* out;
+  long long ldo;
 };
 
 // ---- launchers (templated kernels live in the .cu files) -------------------
 // Z^T = G^T P (n x ldz) with the chunked register-accumulator kernel.
 void launch_compress_stage1(const Pair& pr, const void* g, long long ldg, lsp_dtype gdt,
                             void* zt, cudaStream_t st);
+void launch_compress_stage1_group(const std::vector<S1Job>& jobs, lsp_dtype gdt,
+                                  cudaStream_t st);
+void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t st);
+void compress_group_T(const std::vector<S1Job>& jobs, lsp_dtype gdt, int* flag,
+                      cudaStream_t st);
 // out[r][:] = beta*in[r][:] + alpha * sum_t val[t] * src[idx[t]][:]
 // Rows' entries are [ptr[r], ptr[r+1]) when ptr != nullptr, else [r*k, r*k+k).
 void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const void* val,
@@ -126,6 +152,9 @@ void launch_transpose(int rows, int cols, const void* src, long long lds, void* 
 void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long long ldi,
                        void* out, long long ldo, lsp_dtype dt, double alpha, double beta,
                        const int* skip_flag, DevBuf* partials, int* nparts, cudaStream_t st);
+void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
+                             double beta, const int* skip_flag, DevBuf* partials, int* nparts,
+                             cudaStream_t st);
 void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st);
 void launch_check_finite(size_t cnt, const void* x, lsp_dtype dt, int* flag, cudaStream_t st);
 void launch_convert(size_t cnt, const void* src, lsp_dtype sdt, void* dst, lsp_dtype ddt,
@@ -140,7 +169,7 @@ void launch_refresh_values(const Projector& p, cudaStream_t st);
 
 // High-level building blocks used by the C-ABI.
 void compress_T(Pair& pr, const void* g, long long ldg, lsp_dtype gdt, void* s_t,
-                cudaStream_t st);
+                cudaStream_t st, int* flag = nullptr);
 const void* delta_as_T(Pair& pr, const void* s, lsp_layout layout, cudaStream_t st);
 
 }  // namespace lspb

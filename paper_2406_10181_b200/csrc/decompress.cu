@@ -2,18 +2,22 @@
 // (reference: left_mul/rightT_mul proj/src/projector.cpp:105-117,148-161,
 //  decompress :170-175, apply proj/src/trainer.cpp:190).
 //
-// One CTA owns a band of BN columns of W (and a range of rows):
-//  phase 1  Y_band[a][jj] = sum_l q(j,l) * delta^T[pos_q(j,l)][a]  for all a,
-//           built in shared memory from coalesced rows of the L2-resident
-//           delta^T (d x (BN+1) floats, padded against bank conflicts);
-//  phase 2  every W row i of the range: k conflict-free row gathers
-//           Y_band[pos_p(i,l)][:] and ONE read-modify-write of W[i][band].
-// W is read and written exactly once; delta never leaves L2.
+// Persistent, HBM-streaming design (one CTA per SM, ~190 KB of shared memory):
+//   * W is cut into column bands of BN columns; the work list is the
+//     band-major sequence of (band, 64-row block) tiles, split evenly over the
+//     CTAs (stream-K style), so every SM gets the same number of bytes.
+//   * Y_band[a][jj] = sum_l q(j,l) * delta^T[pos_q(j,l)][a] (all a, the BN
+//     columns of the band) lives in shared memory (d x (BN+1), padded); it is
+//     rebuilt from the L2-resident delta^T only when a CTA enters a new band.
+//   * W tiles (64 rows x BN) and the matching CSR entries of P stream through
+//     a 6-stage cp.async ring, so ~40 KB of W is always in flight per SM
+//     independent of registers, and the first stages are in flight while
+//     Y_band is being built.
+//   * Each W row: k conflict-free gathers Y_band[pos_p(i,l)][:], one
+//     read-modify-write of W[i][band].  W is read and written exactly once.
 #include <algorithm>
 #include <cmath>
-#include <memory>
-#include <mutex>
-#include <vector>
+#include <type_traits>
 
 #include "core.cuh"
 
@@ -22,371 +26,314 @@ namespace lspb {
 namespace {
 
 constexpr int kDecThreads = 512;
-constexpr int kDecUnroll = 4;
+constexpr int kDecWarps = kDecThreads / 32;
+constexpr int kRows = 64;     // W rows per ring stage
+constexpr int kStages = 6;    // ring depth
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
 
 template <typename Tw, typename Tacc, int BN>
-__global__ void __launch_bounds__(kDecThreads)
-    k_decompress_band(int m, int n, int d, int r, const int* __restrict__ ppos,
-                      const Tacc* __restrict__ pval, const int* __restrict__ qpos,
-                      const Tacc* __restrict__ qval, const Tacc* __restrict__ dT, int ldd,
-                      const Tw* in, long long ldi, Tw* out, long long ldo, Tacc alpha, Tacc beta,
-                      int nbands, int rows_per_unit, const int* __restrict__ skip,
-                      double* __restrict__ partials) {
+struct Layout {
+  int d, r;
+  __host__ __device__ int y_bytes() const { return align16(d * (BN + 1) * (int)sizeof(Tacc)); }
+  __host__ __device__ int w_bytes() const { return align16(kRows * BN * (int)sizeof(Tw)); }
+  __host__ __device__ int pos_bytes() const { return align16(kRows * r * 4); }
+  __host__ __device__ int val_bytes() const { return align16(kRows * r * (int)sizeof(Tacc)); }
+  __host__ __device__ int stage_bytes() const { return w_bytes() + pos_bytes() + val_bytes(); }
+  __host__ __device__ int total() const { return y_bytes() + kStages * stage_bytes(); }
+};
+
+struct DecMat {
+  int m, n;
+  const int* ppos;
+  const void* pval;
+  const int* qpos;
+  const void* qval;
+  const void* dT;      // d x d, ld d
+  const void* in;
+  long long ldi;
+  void* out;
+  long long ldo;
+  int row_blocks;      // ceil(m / kRows)
+  long long tile_end;  // exclusive prefix of (band, row block) tiles over the group
+  int vec;             // 16-byte cp.async legal for this matrix's W / P arrays
+};
+struct DecArgs {
+  DecMat mat[kMaxGroup];
+  int count;
+  int d, r;
+  long long total;     // all tiles of the group
+  double alpha, beta;
+  const int* skip;
+  double* partials;
+};
+
+template <typename Tw, typename Tacc, int BN>
+__global__ void __launch_bounds__(kDecThreads, 1) k_decompress_band(const __grid_constant__ DecArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Tacc* Y = reinterpret_cast<Tacc*>(smem_raw);  // [d][BN+1]
+  if (A.skip && *A.skip) return;
+  const Layout<Tw, Tacc, BN> L{A.d, A.r};
   constexpr int LDY = BN + 1;
-  if (skip && *skip) return;
-  const int band = blockIdx.x % nbands, rs = blockIdx.x / nbands;
-  const int j0 = band * BN;
-  const int i_begin = rs * rows_per_unit;
-  const int i_end = min(m, i_begin + rows_per_unit);
-  const int tid = threadIdx.x;
+  Tacc* Y = reinterpret_cast<Tacc*>(smem_raw);
+  unsigned char* ring = smem_raw + L.y_bytes();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = A.d, r = A.r;
+  const Tacc alpha = static_cast<Tacc>(A.alpha), beta = static_cast<Tacc>(A.beta);
 
-  // ---- phase 1: Y_band ----------------------------------------------------
-  for (int jj = 0; jj < BN; ++jj) {
-    const int j = j0 + jj;
-    if (j >= n) {
-      for (int a = tid; a < d; a += kDecThreads) Y[a * LDY + jj] = Tacc(0);
-      continue;
-    }
-    for (int a = tid; a < d; a += kDecThreads) {
-      Tacc y = Tacc(0);
-      for (int l = 0; l < r; ++l) {
-        const int b = qpos[static_cast<long long>(j) * r + l];
-        y = fma(qval[static_cast<long long>(j) * r + l], dT[static_cast<long long>(b) * ldd + a], y);
+  // this CTA's contiguous share of the (matrix, band, row block) tile list
+  const long long t_begin = A.total * blockIdx.x / gridDim.x;
+  const long long t_end = A.total * (blockIdx.x + 1) / gridDim.x;
+  const int ntiles = static_cast<int>(t_end - t_begin);
+
+  auto tile_of = [&](int s, int* mi, int* band, int* r0) {
+    const long long t = t_begin + s;
+    int i = 0;
+    while (i + 1 < A.count && t >= A.mat[i].tile_end) ++i;
+    const long long lt = t - (i ? A.mat[i - 1].tile_end : 0);
+    *mi = i;
+    *band = static_cast<int>(lt / A.mat[i].row_blocks);
+    *r0 = static_cast<int>(lt % A.mat[i].row_blocks) * kRows;
+  };
+
+  // ---- producer: stage s of the ring ---------------------------------------
+  auto issue = [&](int s) {
+    if (s < ntiles) {
+      int mi, band, r0;
+      tile_of(s, &mi, &band, &r0);
+      const DecMat& M = A.mat[mi];
+      const int m = M.m, n = M.n;
+      const Tw* in = static_cast<const Tw*>(M.in);
+      const Tacc* pval = static_cast<const Tacc*>(M.pval);
+      const bool use_in = in != nullptr && A.beta != 0.0;
+      const int j0 = band * BN;
+      const int nrows = min(kRows, m - r0);
+      unsigned char* st = ring + (s % kStages) * L.stage_bytes();
+      Tw* wt = reinterpret_cast<Tw*>(st);
+      int* ps = reinterpret_cast<int*>(st + L.w_bytes());
+      Tacc* vs = reinterpret_cast<Tacc*>(st + L.w_bytes() + L.pos_bytes());
+      if (M.vec) {
+        constexpr int EPP = 16 / sizeof(Tw);  // elements per 16 B piece
+        constexpr int PPR = BN / EPP > 0 ? BN / EPP : 1;
+        if (use_in) {
+          for (int p = tid; p < nrows * PPR; p += kDecThreads) {
+            const int row = p / PPR, pc = p % PPR;
+            const int col = j0 + pc * EPP;
+            const int valid = max(0, min(EPP, n - col));
+            const Tw* src = in + static_cast<long long>(r0 + row) * M.ldi + (valid ? col : 0);
+            cp_async16(wt + row * BN + pc * EPP, src, valid * static_cast<int>(sizeof(Tw)));
+          }
+        }
+        const int pbytes = nrows * r * 4, vbytes = nrows * r * static_cast<int>(sizeof(Tacc));
+        const char* psrc = reinterpret_cast<const char*>(M.ppos + static_cast<long long>(r0) * r);
+        const char* vsrc = reinterpret_cast<const char*>(pval + static_cast<long long>(r0) * r);
+        for (int p = tid; p * 16 < pbytes; p += kDecThreads)
+          cp_async16(reinterpret_cast<char*>(ps) + p * 16, psrc + p * 16, min(16, pbytes - p * 16));
+        for (int p = tid; p * 16 < vbytes; p += kDecThreads)
+          cp_async16(reinterpret_cast<char*>(vs) + p * 16, vsrc + p * 16, min(16, vbytes - p * 16));
+      } else {
+        if (use_in)
+          for (int p = tid; p < nrows * BN; p += kDecThreads) {
+            const int row = p / BN, c = p % BN, col = j0 + c;
+            wt[p] = col < n ? in[static_cast<long long>(r0 + row) * M.ldi + col] : Tw(0.0f);
+          }
+        for (int p = tid; p < nrows * r; p += kDecThreads) {
+          ps[p] = M.ppos[static_cast<long long>(r0) * r + p];
+          vs[p] = pval[static_cast<long long>(r0) * r + p];
+        }
       }
-      Y[a * LDY + jj] = y;
     }
-  }
-  __syncthreads();
+    cp_async_commit();  // always commit: keeps the group count uniform
+  };
 
-  // ---- phase 2: stream W rows ----------------------------------------------
-  constexpr int RPW = 32 / BN;  // rows per warp per iteration
-  const int lane = tid & 31, warp = tid >> 5;
+  // ---- Y_band for band `band` -------------------------------------------------
+  auto build_y = [&](int mi, int band) {
+    const DecMat& M = A.mat[mi];
+    const int n = M.n;
+    const Tacc* qval = static_cast<const Tacc*>(M.qval);
+    const Tacc* dT = static_cast<const Tacc*>(M.dT);
+    const int j0 = band * BN;
+    for (int jj = warp; jj < BN; jj += kDecWarps) {
+      const int j = j0 + jj;
+      for (int a0 = 0; a0 < d; a0 += 32 * 32) {
+        Tacc y[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) y[t] = Tacc(0);
+        if (j < n) {
+          for (int l = 0; l < r; ++l) {
+            const int b = M.qpos[static_cast<long long>(j) * r + l];
+            const Tacc q = qval[static_cast<long long>(j) * r + l];
+            const Tacc* row = dT + static_cast<long long>(b) * d + a0 + lane;
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (a0 + lane + 32 * t < d) y[t] = fma(q, row[32 * t], y[t]);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int a = a0 + lane + 32 * t;
+          if (a < d) Y[a * LDY + jj] = y[t];
+        }
+      }
+    }
+  };
+
+  // ---- consumer -----------------------------------------------------------------
+  constexpr int RPW = 32 / BN;  // rows per warp instruction
   const int jj = lane % BN, rsub = lane / BN;
-  const int j = j0 + jj;
-  const bool col_ok = j < n;
-  const int stride = (kDecThreads / 32) * RPW;
   double ss = 0.0;
-  const bool use_in = in != nullptr && beta != Tacc(0);
-  for (int i0 = i_begin + warp * RPW + rsub; i0 < i_end; i0 += stride * kDecUnroll) {
-    Tw wv[kDecUnroll];
-#pragma unroll
-    for (int u = 0; u < kDecUnroll; ++u) {
-      const int i = i0 + u * stride;
-      if (use_in && col_ok && i < i_end) wv[u] = in[static_cast<long long>(i) * ldi + j];
+
+  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  int cur_band = -1, cur_mat = -1;
+  for (int s = 0; s < ntiles; ++s) {
+    int mi, band, r0;
+    tile_of(s, &mi, &band, &r0);
+    if (band != cur_band || mi != cur_mat) {
+      __syncthreads();  // everyone is done with the previous Y_band
+      build_y(mi, band);
+      cur_band = band;
+      cur_mat = mi;
     }
-#pragma unroll
-    for (int u = 0; u < kDecUnroll; ++u) {
-      const int i = i0 + u * stride;
-      if (i >= i_end) break;
+    const DecMat& M = A.mat[mi];
+    const int m = M.m, n = M.n;
+    const Tw* in = static_cast<const Tw*>(M.in);
+    Tw* out = static_cast<Tw*>(M.out);
+    const bool use_in = in != nullptr && A.beta != 0.0;
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // stage s visible to all; stage s-1 fully consumed
+    issue(s + kStages - 1);
+    const unsigned char* st = ring + (s % kStages) * L.stage_bytes();
+    const Tw* wt = reinterpret_cast<const Tw*>(st);
+    const int* ps = reinterpret_cast<const int*>(st + L.w_bytes());
+    const Tacc* vs = reinterpret_cast<const Tacc*>(st + L.w_bytes() + L.pos_bytes());
+    const int nrows = min(kRows, m - r0);
+    const int j = band * BN + jj;
+    const bool col_ok = j < n;
+    for (int q = warp * RPW + rsub; q < nrows; q += kDecWarps * RPW) {
       Tacc acc = Tacc(0);
-      for (int l = 0; l < r; ++l) {
-        const long long e = static_cast<long long>(i) * r + l;
-        acc = fma(pval[e], Y[ppos[e] * LDY + jj], acc);
-      }
+      for (int l = 0; l < r; ++l) acc = fma(vs[q * r + l], Y[ps[q * r + l] * LDY + jj], acc);
       if (!col_ok) continue;
       Tacc res = alpha * acc;
-      if (use_in) res = fma(beta, cvt<Tacc>(wv[u]), res);
-      if (out) out[static_cast<long long>(i) * ldo + j] = cvt<Tw>(res);
-      if (partials) {
+      if (use_in) res = fma(beta, cvt<Tacc>(wt[q * BN + jj]), res);
+      const long long i = r0 + q;
+      if (out) out[i * M.ldo + j] = cvt<Tw>(res);
+      if (A.partials) {
         const double rv = static_cast<double>(cvt<Tacc>(cvt<Tw>(res)));
         ss += out ? rv * rv : static_cast<double>(res) * static_cast<double>(res);
       }
     }
   }
-  if (partials) {
-    __shared__ double red[kDecThreads / 32];
+  cp_async_wait<0>();
+  if (A.partials) {
+    __shared__ double red[kDecWarps];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    __syncthreads();
     if (lane == 0) red[warp] = ss;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int w = 0; w < kDecThreads / 32; ++w) t += red[w];
-      partials[blockIdx.x] = t;
+      for (int w = 0; w < kDecWarps; ++w) t += red[w];
+      A.partials[blockIdx.x] = t;
     }
   }
 }
 
 template <typename Tw, typename Tacc, int BN>
-void decompress_impl(const Pair& pr, const Tacc* dT, const Tw* in, long long ldi, Tw* out,
-                     long long ldo, double alpha, double beta, const int* skip,
-                     DevBuf* partials, int* nparts, cudaStream_t st) {
-  const int smem = pr.d * (BN + 1) * static_cast<int>(sizeof(Tacc));
+void decompress_impl(const std::vector<DecJob>& jobs, double alpha, double beta,
+                     const int* skip, DevBuf* partials, int* nparts, cudaStream_t st) {
+  const Pair& p0 = *jobs[0].pr;
+  const Layout<Tw, Tacc, BN> L{p0.d, p0.p->r};
+  const int smem = L.total();
   auto kern = k_decompress_band<Tw, Tacc, BN>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int nbands = ceil_div(pr.n, BN);
-  const int per_sm = std::max(1, std::min(4, (220 * 1024) / std::max(smem, 1)));
-  const int target = 2 * per_sm * num_sms();
-  const int max_split = std::max(1, ceil_div(pr.m, 64));
-  const int rsplit = std::max(1, std::min(max_split, ceil_div(target, nbands)));
-  const int rows_per_unit = ceil_div(pr.m, rsplit);
-  const int units = nbands * ceil_div(pr.m, rows_per_unit);
-  if (nparts) *nparts = units;
-  if (partials) partials->ensure(static_cast<size_t>(units) * sizeof(double));
-  double* parts = partials ? partials->as<double>() : nullptr;
-  kern<<<units, kDecThreads, smem, st>>>(pr.m, pr.n, pr.d, pr.p->r, pr.p->pos.as<int>(),
-                                         pr.p->val.as<Tacc>(), pr.q->pos.as<int>(),
-                                         pr.q->val.as<Tacc>(), dT, pr.d, in, ldi, out, ldo,
-                                         static_cast<Tacc>(alpha), static_cast<Tacc>(beta),
-                                         nbands, rows_per_unit, skip, parts);
+  DecArgs A{};
+  A.count = static_cast<int>(jobs.size());
+  A.d = p0.d, A.r = p0.p->r;
+  A.alpha = alpha, A.beta = beta;
+  long long total = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const DecJob& J = jobs[i];
+    const Pair& pr = *J.pr;
+    DecMat& M = A.mat[i];
+    M.m = pr.m, M.n = pr.n;
+    M.ppos = pr.p->pos.as<int>(), M.pval = pr.p->val.p;
+    M.qpos = pr.q->pos.as<int>(), M.qval = pr.q->val.p;
+    M.dT = J.delta_t;
+    M.in = J.in, M.ldi = J.ldi, M.out = J.out, M.ldo = J.ldo;
+    M.row_blocks = ceil_div(pr.m, kRows);
+    total += static_cast<long long>(ceil_div(pr.n, BN)) * M.row_blocks;
+    M.tile_end = total;
+    const bool w_ok = J.in == nullptr ||
+                      (reinterpret_cast<uintptr_t>(J.in) % 16 == 0 &&
+                       (J.ldi * static_cast<long long>(sizeof(Tw))) % 16 == 0);
+    M.vec = (w_ok && reinterpret_cast<uintptr_t>(pr.p->pos.p) % 16 == 0 &&
+             reinterpret_cast<uintptr_t>(pr.p->val.p) % 16 == 0 &&
+             (BN * sizeof(Tw)) % 16 == 0) ? 1 : 0;
+  }
+  A.total = total;
+  A.skip = skip;
+  int per_sm = 0;
+  LSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem));
+  per_sm = std::max(per_sm, 1);
+  const int grid = static_cast<int>(std::min<long long>(total, 1LL * per_sm * num_sms()));
+  if (nparts) *nparts = grid;
+  if (partials) partials->ensure(static_cast<size_t>(grid) * sizeof(double));
+  A.partials = partials ? partials->as<double>() : nullptr;
+  if (grid <= 0) return;
+  kern<<<grid, kDecThreads, smem, st>>>(A);
   after_launch("decompress_band");
 }
 
 }  // namespace
 
-void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long long ldi,
-                       void* out, long long ldo, lsp_dtype dt, double alpha, double beta,
-                       const int* skip_flag, DevBuf* partials, int* nparts, cudaStream_t st) {
-  LSP_DISPATCH_ACC(pr.compute, Tacc, {
+void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
+                             double beta, const int* skip_flag, DevBuf* partials, int* nparts,
+                             cudaStream_t st) {
+  if (nparts) *nparts = 0;
+  if (jobs.empty()) return;
+  require(jobs.size() <= static_cast<size_t>(kMaxGroup), "group too large");
+  const Pair& p0 = *jobs[0].pr;
+  for (const DecJob& J : jobs)
+    require(J.pr->d == p0.d && J.pr->p->r == p0.p->r && J.pr->compute == p0.compute,
+            "decompress group: matrices must share d, r and compute dtype");
+  LSP_DISPATCH_ACC(p0.compute, Tacc, {
     LSP_DISPATCH_STORAGE(dt, Tw, {
-      const size_t budget = 200 * 1024;
-      const size_t row = static_cast<size_t>(pr.d) * sizeof(Tacc);
-      const Tacc* dT = static_cast<const Tacc*>(delta_t);
-      const Tw* pin = static_cast<const Tw*>(in);
-      Tw* pout = static_cast<Tw*>(out);
-      if (row * 33 <= budget)
-        decompress_impl<Tw, Tacc, 32>(pr, dT, pin, ldi, pout, ldo, alpha, beta, skip_flag, partials, nparts, st);
-      else if (row * 17 <= budget)
-        decompress_impl<Tw, Tacc, 16>(pr, dT, pin, ldi, pout, ldo, alpha, beta, skip_flag, partials, nparts, st);
-      else if (row * 9 <= budget)
-        decompress_impl<Tw, Tacc, 8>(pr, dT, pin, ldi, pout, ldo, alpha, beta, skip_flag, partials, nparts, st);
-      else if (row * 5 <= budget)
-        decompress_impl<Tw, Tacc, 4>(pr, dT, pin, ldi, pout, ldo, alpha, beta, skip_flag, partials, nparts, st);
+      constexpr int kBudget = 220 * 1024;
+      const int r = p0.p->r, d = p0.d;
+      if (Layout<Tw, Tacc, 32>{d, r}.total() <= kBudget)
+        decompress_impl<Tw, Tacc, 32>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+      else if (Layout<Tw, Tacc, 16>{d, r}.total() <= kBudget)
+        decompress_impl<Tw, Tacc, 16>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+      else if (Layout<Tw, Tacc, 8>{d, r}.total() <= kBudget)
+        decompress_impl<Tw, Tacc, 8>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+      else if (Layout<Tw, Tacc, 4>{d, r}.total() <= kBudget)
+        decompress_impl<Tw, Tacc, 4>(jobs, alpha, beta, skip_flag, partials, nparts, st);
       else
         fail(LSP_EINVAL, "decompress: subspace width too large for the band kernel");
     })
   })
 }
 
-// ---------------------------------------------------------------------------
-// Subspace Adam (proj/src/subspace_opt.cpp:35-57).  Elementwise, no
-// contraction (explicit _rn ops) so the fp64 path rounds exactly like the
-// reference: m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
-// delta = (m / c1) / (sqrt(v / c2) + eps).
-// ---------------------------------------------------------------------------
-namespace {
-
-__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
-__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
-__device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
-
-// Advances the device step counter (unless a non-finite gradient is latched)
-// and publishes (1 - b1^t, 1 - b2^t).  The corrections come from a host table
-// computed with std::pow, exactly as the reference does (subspace_opt.cpp:44-45).
-__global__ void k_adam_prep(const int* __restrict__ skip, long long* __restrict__ step,
-                            const double2* __restrict__ table, long long cap, double b1,
-                            double b2, double* __restrict__ corr) {
-  if (skip && *skip) return;
-  const long long t = *step + 1;
-  *step = t;
-  double2 c;
-  if (t <= cap) {
-    c = table[t - 1];
-  } else {
-    c.x = 1.0 - pow(b1, static_cast<double>(t));
-    c.y = 1.0 - pow(b2, static_cast<double>(t));
+void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long long ldi,
+                       void* out, long long ldo, lsp_dtype dt, double alpha, double beta,
+                       const int* skip_flag, DevBuf* partials, int* nparts, cudaStream_t st) {
+  if (pr.m <= 0 || pr.n <= 0) {
+    if (nparts) *nparts = 0;
+    return;
   }
-  corr[0] = c.x;
-  corr[1] = c.y;
-}
-
-template <typename T>
-__global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m,
-                       T* __restrict__ v, T* __restrict__ delta, T b1, T omb1, T b2, T omb2,
-                       const double* __restrict__ corr, T eps, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const T c1 = static_cast<T>(corr[0]), c2 = static_cast<T>(corr[1]);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x) {
-    const T gi = g[i];
-    const T mi = add_(mul_(b1, m[i]), mul_(omb1, gi));
-    const T vi = add_(mul_(b2, v[i]), mul_(mul_(omb2, gi), gi));
-    m[i] = mi;
-    v[i] = vi;
-    delta[i] = div_(div_(mi, c1), add_(sqrt_(div_(vi, c2)), eps));
-  }
-}
-
-__device__ __forceinline__ bool finite_val(float v) { return isfinite(v); }
-__device__ __forceinline__ bool finite_val(double v) { return isfinite(v); }
-__device__ __forceinline__ bool finite_val(bf16 v) { return isfinite(__bfloat162float(v)); }
-
-template <typename T>
-__global__ void k_check_finite(long long cnt, const T* __restrict__ x, int* flag) {
-  bool bad = false;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x)
-    bad |= !finite_val(x[i]);
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
-}
-
-template <typename Ts, typename Td>
-__global__ void k_convert(long long cnt, const Ts* __restrict__ s, Td* __restrict__ d) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x)
-    d[i] = cvt<Td>(cvt<double>(s[i]));
-}
-
-template <typename Ts, typename Td>
-__global__ void k_convert2d(int rows, int cols, const Ts* __restrict__ s, long long lds,
-                            Td* __restrict__ d, long long ldd) {
-  const long long cnt = static_cast<long long>(rows) * cols;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / cols, c = i % cols;
-    d[r * ldd + c] = cvt<Td>(cvt<double>(s[r * lds + c]));
-  }
-}
-
-__global__ void k_reduce_partials(const double* __restrict__ p, int n, double* out) {
-  // single block, fixed order -> deterministic
-  __shared__ double red[256];
-  double t = 0.0;
-  for (int i = threadIdx.x; i < n; i += 256) t += p[i];
-  red[threadIdx.x] = t;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < 256; ++i) s += red[i];
-    *out = s;
-  }
-}
-
-template <typename T>
-__global__ void k_gather_values(long long cnt, const int* __restrict__ perm,
-                                const T* __restrict__ src, T* __restrict__ dst) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x)
-    dst[i] = src[perm[i]];
-}
-template <typename E, typename T>
-__global__ void k_gather_entry_values(long long cnt, const int* __restrict__ perm,
-                                      const T* __restrict__ src, E* __restrict__ dst) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x)
-    dst[i].val = src[perm[i]];
-}
-
-int grid_for(long long cnt) {
-  return static_cast<int>(std::max<long long>(1, std::min<long long>((cnt + 255) / 256, 16LL * num_sms())));
-}
-
-}  // namespace
-
-// Bias-correction tables shared by every state with the same betas.
-static const double2* correction_table(double b1, double b2, long long* cap) {
-  struct Entry {
-    double b1, b2;
-    DevBuf buf;
-  };
-  static std::mutex mu;
-  static std::vector<std::unique_ptr<Entry>> cache;
-  constexpr long long kCap = 1LL << 17;
-  std::lock_guard<std::mutex> lock(mu);
-  *cap = kCap;
-  for (auto& e : cache)
-    if (e->b1 == b1 && e->b2 == b2) return e->buf.as<double2>();
-  auto e = std::make_unique<Entry>();
-  e->b1 = b1;
-  e->b2 = b2;
-  std::vector<double2> h(kCap);
-  for (long long t = 1; t <= kCap; ++t)
-    h[t - 1] = make_double2(1.0 - std::pow(b1, static_cast<double>(t)),
-                            1.0 - std::pow(b2, static_cast<double>(t)));
-  e->buf.ensure(kCap * sizeof(double2));
-  LSP_CUDA(cudaMemcpy(e->buf.p, h.data(), kCap * sizeof(double2), cudaMemcpyHostToDevice));
-  cache.push_back(std::move(e));
-  return cache.back()->buf.as<double2>();
-}
-
-void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st) {
-  long long cap = 0;
-  const double2* table = correction_table(a.beta1, a.beta2, &cap);
-  k_adam_prep<<<1, 1, 0, st>>>(skip_flag, a.dstep.as<long long>(), table, cap, a.beta1, a.beta2,
-                               a.corr.as<double>());
-  after_launch("adam_prep");
-  const long long cnt = static_cast<long long>(a.count());
-  LSP_DISPATCH_ACC(a.compute, T, {
-    k_adam<T><<<grid_for(cnt), 256, 0, st>>>(cnt, static_cast<const T*>(grad), a.m.as<T>(),
-                                             a.v.as<T>(), static_cast<T*>(delta), (T)a.beta1,
-                                             (T)(1.0 - a.beta1), (T)a.beta2, (T)(1.0 - a.beta2),
-                                             a.corr.as<double>(), (T)a.eps, skip_flag);
-  })
-  after_launch("adam");
-}
-
-void launch_check_finite(size_t cnt, const void* x, lsp_dtype dt, int* flag, cudaStream_t st) {
-  LSP_DISPATCH_STORAGE(dt, T, {
-    k_check_finite<T><<<grid_for(cnt), 256, 0, st>>>(static_cast<long long>(cnt),
-                                                     static_cast<const T*>(x), flag);
-  })
-  after_launch("check_finite");
-}
-
-void launch_convert(size_t cnt, const void* src, lsp_dtype sdt, void* dst, lsp_dtype ddt,
-                    cudaStream_t st) {
-  LSP_DISPATCH_STORAGE(sdt, Ts, {
-    LSP_DISPATCH_STORAGE(ddt, Td, {
-      k_convert<Ts, Td><<<grid_for(cnt), 256, 0, st>>>(static_cast<long long>(cnt),
-                                                       static_cast<const Ts*>(src),
-                                                       static_cast<Td*>(dst));
-    })
-  })
-  after_launch("convert");
-}
-
-void launch_convert2d(int rows, int cols, const void* src, long long lds, lsp_dtype sdt,
-                      void* dst, long long ldd, lsp_dtype ddt, cudaStream_t st) {
-  const long long cnt = static_cast<long long>(rows) * cols;
-  if (cnt <= 0) return;
-  LSP_DISPATCH_STORAGE(sdt, Ts, {
-    LSP_DISPATCH_STORAGE(ddt, Td, {
-      k_convert2d<Ts, Td><<<grid_for(cnt), 256, 0, st>>>(rows, cols, static_cast<const Ts*>(src),
-                                                         lds, static_cast<Td*>(dst), ldd);
-    })
-  })
-  after_launch("convert2d");
-}
-
-double reduce_partials_sync(const double* partials, int n, cudaStream_t st) {
-  static thread_local DevBuf out;
-  out.ensure(sizeof(double));
-  k_reduce_partials<<<1, 256, 0, st>>>(partials, n, out.as<double>());
-  after_launch("reduce_partials");
-  double h = 0.0;
-  LSP_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-  LSP_CUDA(cudaStreamSynchronize(st));
-  return h;
-}
-
-void launch_refresh_values(const Projector& p, cudaStream_t st) {
-  const long long nnz = static_cast<long long>(p.nnz());
-  LSP_DISPATCH_ACC(p.compute, T, {
-    k_gather_values<T><<<grid_for(nnz), 256, 0, st>>>(nnz, p.csc_perm.as<int>(), p.val.as<T>(),
-                                                      p.csc_val.as<T>());
-    after_launch("refresh_csc");
-    for (const auto& ct : p.chunks) {
-      using E = typename EntryOf<T>::type;
-      k_gather_entry_values<E, T><<<grid_for(nnz), 256, 0, st>>>(nnz, ct->perm.as<int>(),
-                                                                 p.val.as<T>(), ct->ent.as<E>());
-      after_launch("refresh_chunks");
-    }
-  })
-}
-
-// delta given in `layout` -> pointer to delta^T (d x d, ld d) on the device.
-const void* delta_as_T(Pair& pr, const void* s, lsp_layout layout, cudaStream_t st) {
-  if (layout == LSP_LAYOUT_T) return s;
-  pr.d_t.ensure(static_cast<size_t>(pr.d) * pr.d * dtype_size(pr.compute));
-  launch_transpose(pr.d, pr.d, s, pr.d, pr.d_t.p, pr.d, pr.compute, st);
-  return pr.d_t.p;
+  std::vector<DecJob> jobs{DecJob{&pr, delta_t, in, ldi, out, ldo}};
+  launch_decompress_group(jobs, dt, alpha, beta, skip_flag, partials, nparts, st);
 }
 
 }  // namespace lspb

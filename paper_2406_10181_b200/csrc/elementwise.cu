@@ -1,0 +1,242 @@
+// Elementwise / bookkeeping kernels: subspace Adam, non-finite checks, dtype
+// conversion, deterministic reductions and projector value refresh.
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "core.cuh"
+
+namespace lspb {
+
+// ---------------------------------------------------------------------------
+// Subspace Adam (proj/src/subspace_opt.cpp:35-57).  Elementwise, no
+// contraction (explicit _rn ops) so the fp64 path rounds exactly like the
+// reference: m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
+// delta = (m / c1) / (sqrt(v / c2) + eps).
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+
+// Subspace Adam.  Every block reads the step counter, computes the bias
+// corrections (1 - b1^t, 1 - b2^t) from a host table filled with std::pow,
+// exactly like the reference (subspace_opt.cpp:44-45), and the last block to
+// finish advances the counter -- so a captured CUDA graph replays correctly.
+template <typename T>
+__global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m,
+                       T* __restrict__ v, T* __restrict__ delta, T b1, T omb1, T b2, T omb2,
+                       const double2* __restrict__ table, long long cap, double db1,
+                       double db2, T eps, long long* __restrict__ step,
+                       unsigned* __restrict__ done, const int* __restrict__ skip) {
+  if (skip && *skip) return;  // uniform over the grid: nobody touches the counter
+  const long long t = *step + 1;
+  double2 c;
+  if (t <= cap) {
+    c = table[t - 1];
+  } else {
+    c.x = 1.0 - pow(db1, static_cast<double>(t));
+    c.y = 1.0 - pow(db2, static_cast<double>(t));
+  }
+  const T c1 = static_cast<T>(c.x), c2 = static_cast<T>(c.y);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x) {
+    const T gi = g[i];
+    const T mi = add_(mul_(b1, m[i]), mul_(omb1, gi));
+    const T vi = add_(mul_(b2, v[i]), mul_(mul_(omb2, gi), gi));
+    m[i] = mi;
+    v[i] = vi;
+    delta[i] = div_(div_(mi, c1), add_(sqrt_(div_(vi, c2)), eps));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {  // every block has read *step
+      *step = t;
+      *done = 0u;
+      __threadfence();
+    }
+  }
+}
+
+__device__ __forceinline__ bool finite_val(float v) { return isfinite(v); }
+__device__ __forceinline__ bool finite_val(double v) { return isfinite(v); }
+__device__ __forceinline__ bool finite_val(bf16 v) { return isfinite(__bfloat162float(v)); }
+
+template <typename T>
+__global__ void k_check_finite(long long cnt, const T* __restrict__ x, int* flag) {
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    bad |= !finite_val(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+template <typename Ts, typename Td>
+__global__ void k_convert(long long cnt, const Ts* __restrict__ s, Td* __restrict__ d) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = cvt<Td>(cvt<double>(s[i]));
+}
+
+template <typename Ts, typename Td>
+__global__ void k_convert2d(int rows, int cols, const Ts* __restrict__ s, long long lds,
+                            Td* __restrict__ d, long long ldd) {
+  const long long cnt = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    d[r * ldd + c] = cvt<Td>(cvt<double>(s[r * lds + c]));
+  }
+}
+
+__global__ void k_reduce_partials(const double* __restrict__ p, int n, double* out) {
+  // single block, fixed order -> deterministic
+  __shared__ double red[256];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) t += p[i];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 256; ++i) s += red[i];
+    *out = s;
+  }
+}
+
+template <typename T>
+__global__ void k_gather_values(long long cnt, const int* __restrict__ perm,
+                                const T* __restrict__ src, T* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+template <typename E, typename T>
+__global__ void k_gather_entry_values(long long cnt, const int* __restrict__ perm,
+                                      const T* __restrict__ src, E* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i].val = src[perm[i]];
+}
+
+int grid_for(long long cnt) {
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((cnt + 255) / 256, 16LL * num_sms())));
+}
+
+}  // namespace
+
+// Bias-correction tables shared by every state with the same betas.
+static const double2* correction_table(double b1, double b2, long long* cap) {
+  struct Entry {
+    double b1, b2;
+    DevBuf buf;
+  };
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<Entry>> cache;
+  constexpr long long kCap = 1LL << 17;
+  std::lock_guard<std::mutex> lock(mu);
+  *cap = kCap;
+  for (auto& e : cache)
+    if (e->b1 == b1 && e->b2 == b2) return e->buf.as<double2>();
+  auto e = std::make_unique<Entry>();
+  e->b1 = b1;
+  e->b2 = b2;
+  std::vector<double2> h(kCap);
+  for (long long t = 1; t <= kCap; ++t)
+    h[t - 1] = make_double2(1.0 - std::pow(b1, static_cast<double>(t)),
+                            1.0 - std::pow(b2, static_cast<double>(t)));
+  e->buf.ensure(kCap * sizeof(double2));
+  LSP_CUDA(cudaMemcpy(e->buf.p, h.data(), kCap * sizeof(double2), cudaMemcpyHostToDevice));
+  cache.push_back(std::move(e));
+  return cache.back()->buf.as<double2>();
+}
+
+void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st) {
+  long long cap = 0;
+  const double2* table = correction_table(a.beta1, a.beta2, &cap);
+  const long long cnt = static_cast<long long>(a.count());
+  LSP_DISPATCH_ACC(a.compute, T, {
+    k_adam<T><<<grid_for(cnt), 256, 0, st>>>(
+        cnt, static_cast<const T*>(grad), a.m.as<T>(), a.v.as<T>(), static_cast<T*>(delta),
+        (T)a.beta1, (T)(1.0 - a.beta1), (T)a.beta2, (T)(1.0 - a.beta2), table, cap, a.beta1,
+        a.beta2, (T)a.eps, a.dstep.as<long long>(), a.done.as<unsigned>(), skip_flag);
+  })
+  after_launch("adam");
+}
+
+void launch_check_finite(size_t cnt, const void* x, lsp_dtype dt, int* flag, cudaStream_t st) {
+  LSP_DISPATCH_STORAGE(dt, T, {
+    k_check_finite<T><<<grid_for(cnt), 256, 0, st>>>(static_cast<long long>(cnt),
+                                                     static_cast<const T*>(x), flag);
+  })
+  after_launch("check_finite");
+}
+
+void launch_convert(size_t cnt, const void* src, lsp_dtype sdt, void* dst, lsp_dtype ddt,
+                    cudaStream_t st) {
+  LSP_DISPATCH_STORAGE(sdt, Ts, {
+    LSP_DISPATCH_STORAGE(ddt, Td, {
+      k_convert<Ts, Td><<<grid_for(cnt), 256, 0, st>>>(static_cast<long long>(cnt),
+                                                       static_cast<const Ts*>(src),
+                                                       static_cast<Td*>(dst));
+    })
+  })
+  after_launch("convert");
+}
+
+void launch_convert2d(int rows, int cols, const void* src, long long lds, lsp_dtype sdt,
+                      void* dst, long long ldd, lsp_dtype ddt, cudaStream_t st) {
+  const long long cnt = static_cast<long long>(rows) * cols;
+  if (cnt <= 0) return;
+  LSP_DISPATCH_STORAGE(sdt, Ts, {
+    LSP_DISPATCH_STORAGE(ddt, Td, {
+      k_convert2d<Ts, Td><<<grid_for(cnt), 256, 0, st>>>(rows, cols, static_cast<const Ts*>(src),
+                                                         lds, static_cast<Td*>(dst), ldd);
+    })
+  })
+  after_launch("convert2d");
+}
+
+double reduce_partials_sync(const double* partials, int n, cudaStream_t st) {
+  static thread_local DevBuf out;
+  out.ensure(sizeof(double));
+  k_reduce_partials<<<1, 256, 0, st>>>(partials, n, out.as<double>());
+  after_launch("reduce_partials");
+  double h = 0.0;
+  LSP_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  LSP_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+void launch_refresh_values(const Projector& p, cudaStream_t st) {
+  const long long nnz = static_cast<long long>(p.nnz());
+  LSP_DISPATCH_ACC(p.compute, T, {
+    k_gather_values<T><<<grid_for(nnz), 256, 0, st>>>(nnz, p.csc_perm.as<int>(), p.val.as<T>(),
+                                                      p.csc_val.as<T>());
+    after_launch("refresh_csc");
+    for (const auto& ct : p.chunks) {
+      using E = typename EntryOf<T>::type;
+      k_gather_entry_values<E, T><<<grid_for(nnz), 256, 0, st>>>(nnz, ct->perm.as<int>(),
+                                                                 p.val.as<T>(), ct->ent.as<E>());
+      after_launch("refresh_chunks");
+    }
+  })
+}
+
+// delta given in `layout` -> pointer to delta^T (d x d, ld d) on the device.
+const void* delta_as_T(Pair& pr, const void* s, lsp_layout layout, cudaStream_t st) {
+  if (layout == LSP_LAYOUT_T) return s;
+  pr.d_t.ensure(static_cast<size_t>(pr.d) * pr.d * dtype_size(pr.compute));
+  launch_transpose(pr.d, pr.d, s, pr.d, pr.d_t.p, pr.d, pr.compute, st);
+  return pr.d_t.p;
+}
+
+}  // namespace lspb

@@ -11,7 +11,8 @@
 //   A1  = Gp S = P^T (P S)                 (two row gathers)
 //   V   = Q A1^T = (A1 Q^T)^T
 //   D   = Gp S Gq - 2 S ,  D^T = Q^T V - 2 S^T
-//   |B|^2 = <D, S> + |G|^2                 (since P^T G Q = S)
+//   |B|^2 = |P S Q^T - G|^2 evaluated directly by the decompress kernel in
+//           sum-of-squares mode (no m x n write, no cancellation)
 //   dL/dP(i,a) = 2/T [ (P A2)[i,:] . S[a,:]  + X[i,:] . D[a,:] ],  A2 = S Gq, X = G Q
 //   dL/dQ(j,b) = 2/T [ V[j,:] . S^T[b,:]     + Z^T[j,:] . D^T[b,:] ], Z^T = G^T P
 // (derivation in DESIGN.md).  Everything runs in fp64 on shadow fp64 copies of
@@ -265,8 +266,19 @@ struct FitEngine {
     set_values64(*Q, qv, st);
   }
 
-  // S^T (and Z^T in pq.zt) for target i, then D^T; returns |b_i|^2.
-  double eval_target(int i) {
+  // |b_i|^2 = |P S Q^T - G_i|^2 for target i, evaluated directly (no
+  // cancellation): compress, then the decompress kernel in sum-of-squares mode
+  // with in = G, beta = -1 (nothing m x n is written).
+  double bias2(int i) {
+    compress_T(pq, g[i].p, n, LSP_F64, sT.p, st);
+    int np = 0;
+    launch_decompress(pq, sT.p, g[i].p, n, nullptr, 0, LSP_F64, 1.0, -1.0, nullptr, &parts,
+                      &np, st);
+    return reduce_partials_sync(parts.as<double>(), np, st);
+  }
+
+  // Gradient chain for target i: S^T, Z^T (pq.zt), A1, V, D^T.
+  void chain(int i) {
     compress_T(pq, g[i].p, n, LSP_F64, sT.p, st);
     launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);
     csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S     (m x d)
@@ -274,8 +286,6 @@ struct FitEngine {
     launch_transpose(d, d, a1.p, d, a1T.p, d, LSP_F64, st);
     csr_gather(*Q, a1T.as<double>(), d, v.as<double>(), st);       // V  = Q A1^T  (n x d)
     csc_gather(*Q, v.as<double>(), d, dT.as<double>(), st, -2.0, sT.as<double>());  // D^T
-    const double sd = dot_sync(dT.as<double>(), sT.as<double>(), static_cast<long long>(d) * d, parts, st);
-    return std::max(0.0, sd + gnorm2[i]);
   }
 
   // loss = mean_t |b_t|^2 + reg ; rel = mean over nonzero targets of |b_t|/|G_t|
@@ -285,7 +295,7 @@ struct FitEngine {
     double sum = 0.0, rel = 0.0;
     int counted = 0;
     for (int i = 0; i < T; ++i) {
-      const double b2 = eval_target(i);
+      const double b2 = bias2(i);
       sum += b2;
       if (gnorm2[i] > 0.0) {
         rel += std::sqrt(b2) / std::sqrt(gnorm2[i]);
@@ -317,7 +327,7 @@ struct FitEngine {
     x.ensure(static_cast<size_t>(m) * qp.ldz() * 8);
     const double scale = 2.0 / T;
     for (int i = 0; i < T; ++i) {
-      eval_target(i);                                               // S^T, Z^T (pq.zt), A1, V, D^T
+      chain(i);                                                     // S^T, Z^T (pq.zt), A1, V, D^T
       launch_transpose(d, d, dT.p, d, dd.p, d, LSP_F64, st);        // D
       launch_compress_stage1(qp, gT[i].p, m, LSP_F64, x.p, st);     // X = G Q  (m x ldz)
       csr_gather(*Q, sT.as<double>(), d, qs.as<double>(), st);      // Q S^T    (n x d)

@@ -395,6 +395,103 @@ class AdamState:
             pass
 
 
+class Layer:
+    """Per-layer schedule unit: the matrices of one block stepped together with one
+    grouped launch per stage (the body of proj/src/trainer.cpp:186-198).
+
+    The layer owns contiguous S^T / delta^T buffers and all Adam moments, so a
+    data-parallel caller all-reduces ``s_buffer()`` once between ``compress()``
+    and ``update()``.
+    """
+
+    def __init__(self, pairs: Sequence[DevicePair], beta1=0.9, beta2=0.999, eps=1e-8):
+        self.pairs = list(pairs)
+        arr = (C.c_void_p * len(self.pairs))(*[p.handle for p in self.pairs])
+        h = C.c_void_p()
+        lib.layer_create(len(self.pairs), arr, beta1, beta2, eps, C.byref(h))
+        self._h = h
+        self.d = self.pairs[0].d
+        self._bound = [None] * len(self.pairs)
+        self._s_view = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def bind(self, idx: int, g, w):
+        pr = self.pairs[idx]
+        gp, ldg = _check_dev(g, "layer_bind: g", pr.m, pr.n)
+        wp, ldw = _check_dev(w, "layer_bind: w", pr.m, pr.n)
+        lib.layer_bind(self._h, idx, C.c_void_p(gp), ldg, int(_dtype_of(g)), C.c_void_p(wp),
+                       ldw, int(_dtype_of(w)))
+        self._bound[idx] = (g, w)  # keep the tensors alive
+
+    def s_buffer(self):
+        """torch view of the layer's S^T buffer [count, d, d] (device memory owned by the layer)."""
+        if self._s_view is None:
+            torch = _torch()
+            ptr = C.c_void_p()
+            cnt = C.c_int64()
+            lib.layer_s_buffer(self._h, C.byref(ptr), C.byref(cnt))
+            dt = _torch_dtype(self.pairs[0].compute)
+            self._s_view = _device_view(ptr.value, int(cnt.value), dt).view(
+                len(self.pairs), self.d, self.d)
+        return self._s_view
+
+    def compress(self, stream=None):
+        lib.layer_compress(self._h, _stream(stream))
+
+    def update(self, lr: float, check_finite: bool = False, stream=None):
+        lib.layer_update(self._h, float(lr), int(bool(check_finite)), _stream(stream))
+
+    def adam(self, check_finite: bool = False, stream=None):
+        lib.layer_adam(self._h, int(bool(check_finite)), _stream(stream))
+
+    def apply(self, lr: float, stream=None):
+        lib.layer_apply(self._h, float(lr), _stream(stream))
+
+    def step(self, lr: float, stream=None):
+        lib.layer_step(self._h, float(lr), _stream(stream))
+
+    def check(self, stream=None):
+        lib.layer_check(self._h, _stream(stream))
+
+    def adam_get(self, idx: int, layout=Layout.ROW):
+        d = self.d
+        m = np.zeros(d * d)
+        v = np.zeros(d * d)
+        st = C.c_int64()
+        lib.layer_adam_get(self._h, idx, _dptr(m), _dptr(v), C.byref(st), int(layout))
+        return m.reshape(d, d), v.reshape(d, d), st.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.layer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(ptr: int, numel: int, dtype):
+    """A torch tensor aliasing library-owned device memory (no copy, no ownership)."""
+    torch = _torch()
+    if dtype not in (torch.float32, torch.float64):
+        raise InvalidArgument("only fp32/fp64 compute buffers are exposed")
+
+    class _Holder:
+        pass
+
+    h = _Holder()
+    h.__cuda_array_interface__ = {"shape": (numel,),
+                                  "typestr": "<f4" if dtype == torch.float32 else "<f8",
+                                  "data": (ptr, False), "version": 3}
+    return torch.as_tensor(h, device="cuda")
+
+
 def step(pair: DevicePair, adam: AdamState, g, w, lr: float, s_out=None, stream=None):
     """compress -> Adam -> decompress-and-apply for one matrix (trainer.cpp:187-190)."""
     gp, ldg = _check_dev(g, "step: g", pair.m, pair.n)
