@@ -288,41 +288,25 @@ def run_ours(args):
     order = list(reversed(range(L)))  # backward order: last layer's gradients arrive first
 
     stream = torch.cuda.current_stream()
-    ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(L)] for k in ("compress", "adam", "apply")}
+    from paper_2406_10181_b200.schedule import LayerSchedule
+
+    ev = {(ph, li): (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for ph in ("compress", "adam", "apply") for li in range(L)}
+    recording = [False]
+
+    def record(ph, li, when):
+        if recording[0]:
+            ev[(ph, li)][0 if when == "begin" else 1].record(stream)
+
+    # compress(l) -> all-reduce(S_l) async -> finish(l+1): the all-reduce of layer l
+    # overlaps the compress of layer l-1 (paper_2406_10181_b200/schedule.py)
+    sched = LayerSchedule(layers, args.lr, group=dist.group.WORLD if world > 1 else None,
+                          record=record)
 
     def one_step(record=False):
-        """compress(l) -> all-reduce(S_l) -> adam(l) -> apply(l), one layer behind:
-        the all-reduce of layer l overlaps the compress of layer l-1."""
-        pending = None
-        for j, li in enumerate(order):
-            lay = layers[li]
-            if record:
-                ev["compress"][j][0].record(stream)
-            lay.compress()
-            if record:
-                ev["compress"][j][1].record(stream)
-            work = None
-            if world > 1:
-                work = dist.all_reduce(lay.s_buffer(), op=dist.ReduceOp.AVG, async_op=True)
-            if pending is not None:
-                finish(*pending, record)
-            pending = (j, li, work)
-        finish(*pending, record)
-
-    def finish(j, li, work, record):
-        lay = layers[li]
-        if work is not None:
-            work.wait()
-        if record:
-            ev["adam"][j][0].record(stream)
-        lay.adam(check_finite=world > 1)
-        if record:
-            ev["adam"][j][1].record(stream)
-            ev["apply"][j][0].record(stream)
-        lay.apply(args.lr)
-        if record:
-            ev["apply"][j][1].record(stream)
+        recording[0] = record
+        sched.step()
+        recording[0] = False
 
     for _ in range(args.warmup):
         one_step()
@@ -348,9 +332,9 @@ def run_ours(args):
     launches = lsp.launch_count() - launches0
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
-    comp_ms = [a.elapsed_time(b) for a, b in ev["compress"]]
-    adam_ms = [a.elapsed_time(b) for a, b in ev["adam"]]
-    app_ms = [a.elapsed_time(b) for a, b in ev["apply"]]
+    comp_ms = [ev[("compress", li)][0].elapsed_time(ev[("compress", li)][1]) for li in range(L)]
+    adam_ms = [ev[("adam", li)][0].elapsed_time(ev[("adam", li)][1]) for li in range(L)]
+    app_ms = [ev[("apply", li)][0].elapsed_time(ev[("apply", li)][1]) for li in range(L)]
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

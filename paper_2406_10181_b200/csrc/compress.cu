@@ -31,30 +31,29 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Load rows [row0, row0+BM) x cols [j0, j0+32) of G into a BM x 32 tile.
+// Load rows [row0, row0+bm) x cols [j0, j0+32) of G into a bm x 32 tile.
 // Rows >= m are skipped (never referenced); columns >= n are zero-filled.
-template <typename Tin, int BM, int NT>
+template <typename Tin, int NT>
 __device__ __forceinline__ void load_tile(Tin* tile, const Tin* __restrict__ g, long long ldg,
-                                          int m, int n, int row0, int j0, bool vec) {
+                                          int m, int n, int row0, int j0, int bm, bool vec) {
   constexpr int kPer16 = 16 / sizeof(Tin);       // elements per 16 B
   constexpr int kPieces = 32 / kPer16;           // 16 B pieces per tile row
   const int tid = threadIdx.x;
+  const int rows = min(bm, m - row0);
   if (vec) {
 #pragma unroll 4
-    for (int p = tid; p < BM * kPieces; p += NT) {
+    for (int p = tid; p < rows * kPieces; p += NT) {
       const int row = p / kPieces, piece = p % kPieces;
-      const int gr = row0 + row, gc = j0 + piece * kPer16;
-      if (gr >= m) continue;
+      const int gc = j0 + piece * kPer16;
       const int valid = min(kPer16, n - gc);
-      const Tin* src = g + static_cast<long long>(gr) * ldg + (valid > 0 ? gc : 0);
+      const Tin* src = g + static_cast<long long>(row0 + row) * ldg + (valid > 0 ? gc : 0);
       cp_async16(tile + row * 32 + piece * kPer16, src, valid > 0 ? valid * (int)sizeof(Tin) : 0);
     }
   } else {
-    for (int p = tid; p < BM * 32; p += NT) {
+    for (int p = tid; p < rows * 32; p += NT) {
       const int row = p >> 5, col = p & 31;
-      const int gr = row0 + row, gc = j0 + col;
-      if (gr >= m) continue;
-      tile[p] = gc < n ? g[static_cast<long long>(gr) * ldg + gc] : Tin(0.0f);
+      const int gc = j0 + col;
+      tile[p] = gc < n ? g[static_cast<long long>(row0 + row) * ldg + gc] : Tin(0.0f);
     }
   }
 }
@@ -76,15 +75,21 @@ struct S1Args {
   S1Mat mat[kMaxGroup];
   int count;
   int d;
+  int r;
+  int bm;           // rows per chunk (the chunk tables were built for it)
+  int tile_bytes;   // per-stage G tile bytes (16-aligned)
+  int ent_bytes;    // per-stage entry bytes (16-aligned)
 };
 
-// One CTA = one band of 32 columns of one matrix x (WARPS*32) bins.
-template <typename Tin, typename Tacc, int WARPS, int BM>
+// One CTA = one band of 32 columns of one matrix x (WARPS*32) bins.  Per row
+// chunk, the G tile AND the chunk's CSC(P) entries are staged into shared
+// memory by cp.async (double buffered), so the inner loop has no global loads.
+template <typename Tin, typename Tacc, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_constant__ S1Args A) {
   using Ent = typename EntryOf<Tacc>::type;
   constexpr int NT = WARPS * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Tin* tiles = reinterpret_cast<Tin*>(smem_raw);  // [2][BM][32]
+  const int stage_bytes = A.tile_bytes + A.ent_bytes;
   // which matrix / band (uniform scan over <= kMaxGroup entries)
   int mi = 0;
   while (mi + 1 < A.count && static_cast<int>(blockIdx.x) >= A.mat[mi].band_end) ++mi;
@@ -93,42 +98,61 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
   const Tin* __restrict__ g = static_cast<const Tin*>(M.g);
   const Ent* __restrict__ ent = static_cast<const Ent*>(M.ent);
   const int* __restrict__ split = M.split;
-  const int d = A.d, m = M.m, n = M.n;
+  const int d = A.d, m = M.m, n = M.n, bm = A.bm, r = A.r;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j0 = band * 32;
   const int bin0 = blockIdx.y * NT + warp * 32;
   const int my_bin = bin0 + lane;
   const bool vec16 = M.vec != 0;
 
+  auto stage = [&](int c, int buf) {
+    unsigned char* base = smem_raw + buf * stage_bytes;
+    load_tile<Tin, NT>(reinterpret_cast<Tin*>(base), g, M.ldg, m, n, c * bm, j0, bm, vec16);
+    // the chunk's entries: [c*bm*r, c*bm*r + rows*r), contiguous in the table
+    const long long e0 = static_cast<long long>(c) * bm * r;
+    const int bytes = min(bm, m - c * bm) * r * static_cast<int>(sizeof(Ent));
+    const char* src = reinterpret_cast<const char*>(ent + e0);
+    char* dst = reinterpret_cast<char*>(base + A.tile_bytes);
+    for (int p = threadIdx.x * 16; p < bytes; p += NT * 16) cp_async16(dst + p, src + p, min(16, bytes - p));
+  };
+
   Tacc acc[32];
 #pragma unroll
   for (int b = 0; b < 32; ++b) acc[b] = Tacc(0);
 
-  load_tile<Tin, BM, NT>(tiles, g, M.ldg, m, n, 0, j0, vec16);
+  stage(0, 0);
   cp_async_commit();
   for (int c = 0; c < M.nchunks; ++c) {
     // Chunk c+1 goes to the other buffer; the barrier below the wait also
     // guarantees every warp has finished reading it (chunk c-1).
     cp_async_wait<0>();
     __syncthreads();
-    if (c + 1 < M.nchunks)
-      load_tile<Tin, BM, NT>(tiles + ((c + 1) & 1) * BM * 32, g, M.ldg, m, n, (c + 1) * BM, j0,
-                             vec16);
+    if (c + 1 < M.nchunks) stage(c + 1, (c + 1) & 1);
     cp_async_commit();
-    const Tin* t = tiles + (c & 1) * BM * 32 + lane;
+    const unsigned char* base = smem_raw + (c & 1) * stage_bytes;
+    const Tin* t = reinterpret_cast<const Tin*>(base) + lane;
+    const Ent* E = reinterpret_cast<const Ent*>(base + A.tile_bytes) -
+                   static_cast<long long>(c) * bm * r;  // indexed by global entry id
     // Entries of (chunk c, bin) are contiguous and bins follow each other, so
     // bin b's range is [end(b-1), end(b)).
-    const long long base = static_cast<long long>(c) * d;
-    int e = __ldg(split + base + min(bin0, d));
-    const int my_end = __ldg(split + base + min(my_bin + 1, d));
+    const long long sbase = static_cast<long long>(c) * d;
+    int e = __ldg(split + sbase + min(bin0, d));
+    const int my_end = __ldg(split + sbase + min(my_bin + 1, d));
 #pragma unroll
     for (int b = 0; b < 32; ++b) {
       const int end = __shfl_sync(0xffffffffu, my_end, b);
       Tacc a = acc[b];
 #pragma unroll 1
-      for (; e < end; ++e) {
-        const Ent en = ent[e];
-        a = fma(en.val, cvt<Tacc>(t[en.off]), a);
+      for (; e + 1 < end; e += 2) {
+        const Ent e0 = E[e], e1 = E[e + 1];
+        const Tacc g0 = cvt<Tacc>(t[e0.off]), g1 = cvt<Tacc>(t[e1.off]);
+        a = fma(e0.val, g0, a);
+        a = fma(e1.val, g1, a);
+      }
+      if (e < end) {
+        const Ent e0 = E[e];
+        a = fma(e0.val, cvt<Tacc>(t[e0.off]), a);
+        ++e;
       }
       acc[b] = a;
     }
@@ -151,15 +175,25 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
 
 template <typename Tin, typename Tacc, int WARPS>
 void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
-  constexpr int kStageBytes = WARPS >= 16 ? (sizeof(Tin) == 4 ? 98304 : 65536) : 32768;
-  constexpr int BM = kStageBytes / (32 * sizeof(Tin));
+  using Ent = typename EntryOf<Tacc>::type;
+  const int r = jobs[0].pr->p->r;
+  // Per-stage budget: ~100 KB (two stages fit the 227 KB of an SM) for the
+  // 32-warp kernel, half that for smaller CTAs so several fit per SM.
+  const int budget = WARPS >= 16 ? 100 * 1024 : 48 * 1024;
+  const int row_bytes = 32 * static_cast<int>(sizeof(Tin)) + r * static_cast<int>(sizeof(Ent));
+  const int bm = std::max(32, (budget / row_bytes) / 32 * 32);
   S1Args A{};
   A.count = static_cast<int>(jobs.size());
   A.d = d;
+  A.r = r;
+  A.bm = bm;
+  A.tile_bytes = static_cast<int>(round_up(static_cast<long long>(bm) * 32 * sizeof(Tin), 16));
+  A.ent_bytes = static_cast<int>(round_up(static_cast<long long>(bm) * r * sizeof(Ent), 16));
   int bands = 0;
   for (size_t i = 0; i < jobs.size(); ++i) {
     const S1Job& J = jobs[i];
-    const ChunkTable& ct = J.pr->p->chunk_table(BM);
+    require(J.pr->p->r == r, "compress group: projectors must share r");
+    const ChunkTable& ct = J.pr->p->chunk_table(bm);
     S1Mat& M = A.mat[i];
     M.g = J.g, M.ldg = J.ldg, M.m = J.pr->m, M.n = J.pr->n;
     M.split = ct.split.as<int>(), M.ent = ct.ent.p, M.nchunks = ct.nchunks;
@@ -171,8 +205,8 @@ void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
   }
   if (bands == 0) return;
   dim3 grid(bands, ceil_div(d, WARPS * 32));
-  const int smem = 2 * BM * 32 * sizeof(Tin);
-  auto kern = k_compress_stage1<Tin, Tacc, WARPS, BM>;
+  const int smem = 2 * (A.tile_bytes + A.ent_bytes);
+  auto kern = k_compress_stage1<Tin, Tacc, WARPS>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, WARPS * 32, smem, st>>>(A);
   after_launch("compress_stage1");
@@ -180,7 +214,7 @@ void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
 
 }  // namespace
 
-// Z^T_i = G_i^T P_i for every job of a group (same d, compute and G dtype).
+// Z^T_i = G_i^T P_i for every job of a group (same d, r, compute and G dtype).
 void launch_compress_stage1_group(const std::vector<S1Job>& jobs, lsp_dtype gdt,
                                   cudaStream_t st) {
   if (jobs.empty()) return;

@@ -66,6 +66,7 @@ struct DecMat {
   void* out;
   long long ldo;
   int row_blocks;      // ceil(m / kRows)
+  int nbands;          // ceil(n / BN)
   long long tile_end;  // exclusive prefix of (band, row block) tiles over the group
   int vec;             // 16-byte cp.async legal for this matrix's W / P arrays
 };
@@ -75,91 +76,114 @@ struct DecArgs {
   int d, r;
   long long total;     // all tiles of the group
   double alpha, beta;
+  int use_in;          // beta != 0 and every matrix has an input
   const int* skip;
   double* partials;
 };
 
-template <typename Tw, typename Tacc, int BN>
+// Position in the group's (matrix, band, row block) tile list, advanced one
+// tile at a time (no divisions in the loop).
+struct Cursor {
+  int mi, band, rb;
+};
+
+__device__ __forceinline__ Cursor cursor_at(const DecArgs& A, long long t) {
+  int i = 0;
+  while (i + 1 < A.count && t >= A.mat[i].tile_end) ++i;
+  const long long lt = t - (i ? A.mat[i - 1].tile_end : 0);
+  return Cursor{i, static_cast<int>(lt / A.mat[i].row_blocks),
+                static_cast<int>(lt % A.mat[i].row_blocks)};
+}
+
+__device__ __forceinline__ void advance(const DecArgs& A, Cursor& c) {
+  if (++c.rb == A.mat[c.mi].row_blocks) {
+    c.rb = 0;
+    if (++c.band == A.mat[c.mi].nbands) {
+      c.band = 0;
+      ++c.mi;
+    }
+  }
+}
+
+// KR: nonzeros per projector row known at compile time (0 = runtime A.r).
+template <typename Tw, typename Tacc, int BN, int KR, bool SUMSQ>
 __global__ void __launch_bounds__(kDecThreads, 1) k_decompress_band(const __grid_constant__ DecArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (A.skip && *A.skip) return;
-  const Layout<Tw, Tacc, BN> L{A.d, A.r};
+  const int r = KR > 0 ? KR : A.r;
+  const Layout<Tw, Tacc, BN> L{A.d, r};
   constexpr int LDY = BN + 1;
   Tacc* Y = reinterpret_cast<Tacc*>(smem_raw);
   unsigned char* ring = smem_raw + L.y_bytes();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int d = A.d, r = A.r;
+  const int d = A.d;
   const Tacc alpha = static_cast<Tacc>(A.alpha), beta = static_cast<Tacc>(A.beta);
+  const bool use_in = A.use_in != 0;
 
   // this CTA's contiguous share of the (matrix, band, row block) tile list
   const long long t_begin = A.total * blockIdx.x / gridDim.x;
   const long long t_end = A.total * (blockIdx.x + 1) / gridDim.x;
   const int ntiles = static_cast<int>(t_end - t_begin);
+  if (ntiles <= 0) return;
 
-  auto tile_of = [&](int s, int* mi, int* band, int* r0) {
-    const long long t = t_begin + s;
-    int i = 0;
-    while (i + 1 < A.count && t >= A.mat[i].tile_end) ++i;
-    const long long lt = t - (i ? A.mat[i - 1].tile_end : 0);
-    *mi = i;
-    *band = static_cast<int>(lt / A.mat[i].row_blocks);
-    *r0 = static_cast<int>(lt % A.mat[i].row_blocks) * kRows;
-  };
+  // W piece this thread copies in every stage (fixed row / 16-byte column piece)
+  constexpr int EPP = 16 / sizeof(Tw);
+  constexpr int PPR = BN / EPP > 0 ? BN / EPP : 1;
+  constexpr int kPieces = kRows * PPR;
+  const int my_row = tid / PPR, my_pc = tid % PPR;
 
-  // ---- producer: stage s of the ring ---------------------------------------
+  // ---- producer -------------------------------------------------------------
+  Cursor ic = cursor_at(A, t_begin);
   auto issue = [&](int s) {
     if (s < ntiles) {
-      int mi, band, r0;
-      tile_of(s, &mi, &band, &r0);
-      const DecMat& M = A.mat[mi];
-      const int m = M.m, n = M.n;
-      const Tw* in = static_cast<const Tw*>(M.in);
-      const Tacc* pval = static_cast<const Tacc*>(M.pval);
-      const bool use_in = in != nullptr && A.beta != 0.0;
-      const int j0 = band * BN;
-      const int nrows = min(kRows, m - r0);
+      const DecMat& M = A.mat[ic.mi];
+      const int r0 = ic.rb * kRows, j0 = ic.band * BN;
+      const int nrows = min(kRows, M.m - r0);
       unsigned char* st = ring + (s % kStages) * L.stage_bytes();
       Tw* wt = reinterpret_cast<Tw*>(st);
       int* ps = reinterpret_cast<int*>(st + L.w_bytes());
       Tacc* vs = reinterpret_cast<Tacc*>(st + L.w_bytes() + L.pos_bytes());
+      const Tw* in = static_cast<const Tw*>(M.in);
       if (M.vec) {
-        constexpr int EPP = 16 / sizeof(Tw);  // elements per 16 B piece
-        constexpr int PPR = BN / EPP > 0 ? BN / EPP : 1;
         if (use_in) {
-          for (int p = tid; p < nrows * PPR; p += kDecThreads) {
-            const int row = p / PPR, pc = p % PPR;
-            const int col = j0 + pc * EPP;
-            const int valid = max(0, min(EPP, n - col));
-            const Tw* src = in + static_cast<long long>(r0 + row) * M.ldi + (valid ? col : 0);
-            cp_async16(wt + row * BN + pc * EPP, src, valid * static_cast<int>(sizeof(Tw)));
+#pragma unroll
+          for (int p = 0; p < kPieces; p += kDecThreads) {
+            const int row = my_row + p / PPR;
+            if (p + tid < kPieces && row < nrows) {
+              const int col = j0 + my_pc * EPP;
+              const int valid = max(0, min(EPP, M.n - col));
+              const Tw* src = in + static_cast<long long>(r0 + row) * M.ldi + (valid ? col : 0);
+              cp_async16(wt + row * BN + my_pc * EPP, src, valid * static_cast<int>(sizeof(Tw)));
+            }
           }
         }
         const int pbytes = nrows * r * 4, vbytes = nrows * r * static_cast<int>(sizeof(Tacc));
         const char* psrc = reinterpret_cast<const char*>(M.ppos + static_cast<long long>(r0) * r);
-        const char* vsrc = reinterpret_cast<const char*>(pval + static_cast<long long>(r0) * r);
-        for (int p = tid; p * 16 < pbytes; p += kDecThreads)
-          cp_async16(reinterpret_cast<char*>(ps) + p * 16, psrc + p * 16, min(16, pbytes - p * 16));
-        for (int p = tid; p * 16 < vbytes; p += kDecThreads)
-          cp_async16(reinterpret_cast<char*>(vs) + p * 16, vsrc + p * 16, min(16, vbytes - p * 16));
+        const char* vsrc = reinterpret_cast<const char*>(static_cast<const Tacc*>(M.pval) +
+                                                         static_cast<long long>(r0) * r);
+        for (int p = tid * 16; p < pbytes; p += kDecThreads * 16)
+          cp_async16(reinterpret_cast<char*>(ps) + p, psrc + p, min(16, pbytes - p));
+        for (int p = tid * 16; p < vbytes; p += kDecThreads * 16)
+          cp_async16(reinterpret_cast<char*>(vs) + p, vsrc + p, min(16, vbytes - p));
       } else {
         if (use_in)
           for (int p = tid; p < nrows * BN; p += kDecThreads) {
             const int row = p / BN, c = p % BN, col = j0 + c;
-            wt[p] = col < n ? in[static_cast<long long>(r0 + row) * M.ldi + col] : Tw(0.0f);
+            wt[p] = col < M.n ? in[static_cast<long long>(r0 + row) * M.ldi + col] : Tw(0.0f);
           }
+        const Tacc* pval = static_cast<const Tacc*>(M.pval);
         for (int p = tid; p < nrows * r; p += kDecThreads) {
           ps[p] = M.ppos[static_cast<long long>(r0) * r + p];
           vs[p] = pval[static_cast<long long>(r0) * r + p];
         }
       }
+      advance(A, ic);
     }
     cp_async_commit();  // always commit: keeps the group count uniform
   };
 
-  // ---- Y_band for band `band` -------------------------------------------------
-  auto build_y = [&](int mi, int band) {
-    const DecMat& M = A.mat[mi];
-    const int n = M.n;
+  // ---- Y_band for (matrix, band) -----------------------------------------------
+  auto build_y = [&](const DecMat& M, int band) {
     const Tacc* qval = static_cast<const Tacc*>(M.qval);
     const Tacc* dT = static_cast<const Tacc*>(M.dT);
     const int j0 = band * BN;
@@ -169,10 +193,10 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decompress_band(const __grid
         Tacc y[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) y[t] = Tacc(0);
-        if (j < n) {
+        if (j < M.n) {
           for (int l = 0; l < r; ++l) {
-            const int b = M.qpos[static_cast<long long>(j) * r + l];
-            const Tacc q = qval[static_cast<long long>(j) * r + l];
+            const int b = __ldg(M.qpos + static_cast<long long>(j) * r + l);
+            const Tacc q = __ldg(qval + static_cast<long long>(j) * r + l);
             const Tacc* row = dT + static_cast<long long>(b) * d + a0 + lane;
 #pragma unroll
             for (int t = 0; t < 32; ++t)
@@ -194,21 +218,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decompress_band(const __grid
   double ss = 0.0;
 
   for (int s = 0; s < kStages - 1; ++s) issue(s);
+  Cursor cc = cursor_at(A, t_begin);
   int cur_band = -1, cur_mat = -1;
-  for (int s = 0; s < ntiles; ++s) {
-    int mi, band, r0;
-    tile_of(s, &mi, &band, &r0);
-    if (band != cur_band || mi != cur_mat) {
+  for (int s = 0; s < ntiles; ++s, advance(A, cc)) {
+    const DecMat& M = A.mat[cc.mi];
+    if (cc.band != cur_band || cc.mi != cur_mat) {
       __syncthreads();  // everyone is done with the previous Y_band
-      build_y(mi, band);
-      cur_band = band;
-      cur_mat = mi;
+      build_y(M, cc.band);
+      cur_band = cc.band;
+      cur_mat = cc.mi;
     }
-    const DecMat& M = A.mat[mi];
-    const int m = M.m, n = M.n;
-    const Tw* in = static_cast<const Tw*>(M.in);
-    Tw* out = static_cast<Tw*>(M.out);
-    const bool use_in = in != nullptr && A.beta != 0.0;
     cp_async_wait<kStages - 2>();
     __syncthreads();  // stage s visible to all; stage s-1 fully consumed
     issue(s + kStages - 1);
@@ -216,25 +235,45 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decompress_band(const __grid
     const Tw* wt = reinterpret_cast<const Tw*>(st);
     const int* ps = reinterpret_cast<const int*>(st + L.w_bytes());
     const Tacc* vs = reinterpret_cast<const Tacc*>(st + L.w_bytes() + L.pos_bytes());
-    const int nrows = min(kRows, m - r0);
-    const int j = band * BN + jj;
-    const bool col_ok = j < n;
+    const int r0 = cc.rb * kRows;
+    const int nrows = min(kRows, M.m - r0);
+    const int j = cc.band * BN + jj;
+    const bool col_ok = j < M.n;
+    Tw* out = static_cast<Tw*>(M.out);
+    const long long ldo = M.ldo;
+    Tw* orow = out ? out + static_cast<long long>(r0) * ldo + j : nullptr;
+#pragma unroll 2
     for (int q = warp * RPW + rsub; q < nrows; q += kDecWarps * RPW) {
       Tacc acc = Tacc(0);
-      for (int l = 0; l < r; ++l) acc = fma(vs[q * r + l], Y[ps[q * r + l] * LDY + jj], acc);
+      if constexpr (KR == 4 && sizeof(Tacc) == 4) {
+        const int4 pp = *reinterpret_cast<const int4*>(ps + q * 4);
+        const float4 vv = *reinterpret_cast<const float4*>(vs + q * 4);
+        acc = fma(vv.x, Y[pp.x * LDY + jj], acc);
+        acc = fma(vv.y, Y[pp.y * LDY + jj], acc);
+        acc = fma(vv.z, Y[pp.z * LDY + jj], acc);
+        acc = fma(vv.w, Y[pp.w * LDY + jj], acc);
+      } else {
+#pragma unroll
+        for (int l = 0; l < (KR > 0 ? KR : 1); ++l) {
+          if (KR > 0 || l < r) acc = fma(vs[q * r + l], Y[ps[q * r + l] * LDY + jj], acc);
+        }
+        if constexpr (KR == 0) {
+          for (int l = 1; l < r; ++l) acc = fma(vs[q * r + l], Y[ps[q * r + l] * LDY + jj], acc);
+        }
+      }
       if (!col_ok) continue;
       Tacc res = alpha * acc;
       if (use_in) res = fma(beta, cvt<Tacc>(wt[q * BN + jj]), res);
-      const long long i = r0 + q;
-      if (out) out[i * M.ldo + j] = cvt<Tw>(res);
-      if (A.partials) {
-        const double rv = static_cast<double>(cvt<Tacc>(cvt<Tw>(res)));
-        ss += out ? rv * rv : static_cast<double>(res) * static_cast<double>(res);
+      if (orow) orow[q * ldo] = cvt<Tw>(res);
+      if constexpr (SUMSQ) {
+        const double rv = orow ? static_cast<double>(cvt<Tacc>(cvt<Tw>(res)))
+                               : static_cast<double>(res);
+        ss += rv * rv;
       }
     }
   }
   cp_async_wait<0>();
-  if (A.partials) {
+  if constexpr (SUMSQ) {
     __shared__ double red[kDecWarps];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -249,13 +288,13 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decompress_band(const __grid
   }
 }
 
-template <typename Tw, typename Tacc, int BN>
+template <typename Tw, typename Tacc, int BN, int KR, bool SUMSQ>
 void decompress_impl(const std::vector<DecJob>& jobs, double alpha, double beta,
                      const int* skip, DevBuf* partials, int* nparts, cudaStream_t st) {
   const Pair& p0 = *jobs[0].pr;
   const Layout<Tw, Tacc, BN> L{p0.d, p0.p->r};
   const int smem = L.total();
-  auto kern = k_decompress_band<Tw, Tacc, BN>;
+  auto kern = k_decompress_band<Tw, Tacc, BN, KR, SUMSQ>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   DecArgs A{};
   A.count = static_cast<int>(jobs.size());
@@ -272,7 +311,8 @@ void decompress_impl(const std::vector<DecJob>& jobs, double alpha, double beta,
     M.dT = J.delta_t;
     M.in = J.in, M.ldi = J.ldi, M.out = J.out, M.ldo = J.ldo;
     M.row_blocks = ceil_div(pr.m, kRows);
-    total += static_cast<long long>(ceil_div(pr.n, BN)) * M.row_blocks;
+    M.nbands = ceil_div(pr.n, BN);
+    total += static_cast<long long>(M.nbands) * M.row_blocks;
     M.tile_end = total;
     const bool w_ok = J.in == nullptr ||
                       (reinterpret_cast<uintptr_t>(J.in) % 16 == 0 &&
@@ -283,13 +323,15 @@ void decompress_impl(const std::vector<DecJob>& jobs, double alpha, double beta,
   }
   A.total = total;
   A.skip = skip;
+  A.use_in = beta != 0.0;
+  for (const DecJob& J : jobs) A.use_in = A.use_in && J.in != nullptr;
   int per_sm = 0;
   LSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem));
   per_sm = std::max(per_sm, 1);
   const int grid = static_cast<int>(std::min<long long>(total, 1LL * per_sm * num_sms()));
   if (nparts) *nparts = grid;
-  if (partials) partials->ensure(static_cast<size_t>(grid) * sizeof(double));
-  A.partials = partials ? partials->as<double>() : nullptr;
+  if (SUMSQ) partials->ensure(static_cast<size_t>(grid) * sizeof(double));
+  A.partials = SUMSQ ? partials->as<double>() : nullptr;
   if (grid <= 0) return;
   kern<<<grid, kDecThreads, smem, st>>>(A);
   after_launch("decompress_band");
@@ -311,14 +353,24 @@ void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, doub
     LSP_DISPATCH_STORAGE(dt, Tw, {
       constexpr int kBudget = 220 * 1024;
       const int r = p0.p->r, d = p0.d;
+      auto run = [&](auto bn) {
+        constexpr int BN = decltype(bn)::value;
+        if (partials) {
+          decompress_impl<Tw, Tacc, BN, 0, true>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        } else if (r == 4) {
+          decompress_impl<Tw, Tacc, BN, 4, false>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        } else {
+          decompress_impl<Tw, Tacc, BN, 0, false>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        }
+      };
       if (Layout<Tw, Tacc, 32>{d, r}.total() <= kBudget)
-        decompress_impl<Tw, Tacc, 32>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        run(std::integral_constant<int, 32>{});
       else if (Layout<Tw, Tacc, 16>{d, r}.total() <= kBudget)
-        decompress_impl<Tw, Tacc, 16>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        run(std::integral_constant<int, 16>{});
       else if (Layout<Tw, Tacc, 8>{d, r}.total() <= kBudget)
-        decompress_impl<Tw, Tacc, 8>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        run(std::integral_constant<int, 8>{});
       else if (Layout<Tw, Tacc, 4>{d, r}.total() <= kBudget)
-        decompress_impl<Tw, Tacc, 4>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+        run(std::integral_constant<int, 4>{});
       else
         fail(LSP_EINVAL, "decompress: subspace width too large for the band kernel");
     })
