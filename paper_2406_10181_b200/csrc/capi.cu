@@ -76,11 +76,12 @@ void Projector::upload_values() {
 
 void Projector::refresh_values(cudaStream_t st) { launch_refresh_values(*this, st); }
 
-const ChunkTable& Projector::chunk_table(int bm) {
+const ChunkTable& Projector::chunk_table(int bm, int esize) {
   for (auto& c : chunks)
-    if (c->bm == bm) return *c;
+    if (c->bm == bm && c->esize == esize) return *c;
   auto ct = std::make_unique<ChunkTable>();
   ct->bm = bm;
+  ct->esize = esize;
   ct->nchunks = ceil_div(n_rows, bm);
   std::vector<int32_t> split, rows, perm;
   build_chunks(n_rows, d, bm, h_csc_ptr, h_csc_rows, h_csc_perm, split, rows, perm);
@@ -91,7 +92,7 @@ const ChunkTable& Projector::chunk_table(int bm) {
     std::vector<E> ent(rows.size());
     for (size_t t = 0; t < rows.size(); ++t) {
       ent[t] = E{};
-      ent[t].off = rows[t] * 32;
+      ent[t].off = rows[t] * 32 * esize;
       ent[t].val = static_cast<T>(h_val[perm[t]]);
     }
     upload(ct->ent, ent.data(), ent.size() * sizeof(E));

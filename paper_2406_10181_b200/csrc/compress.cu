@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
     if (c + 1 < M.nchunks) stage(c + 1, (c + 1) & 1);
     cp_async_commit();
     const unsigned char* base = smem_raw + (c & 1) * stage_bytes;
-    const Tin* t = reinterpret_cast<const Tin*>(base) + lane;
+    const unsigned char* tb = base + lane * sizeof(Tin);  // + entry byte offset = G[row][lane]
     const Ent* E = reinterpret_cast<const Ent*>(base + A.tile_bytes) -
                    static_cast<long long>(c) * bm * r;  // indexed by global entry id
     // Entries of (chunk c, bin) are contiguous and bins follow each other, so
@@ -145,13 +145,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
 #pragma unroll 1
       for (; e + 1 < end; e += 2) {
         const Ent e0 = E[e], e1 = E[e + 1];
-        const Tacc g0 = cvt<Tacc>(t[e0.off]), g1 = cvt<Tacc>(t[e1.off]);
+        const Tacc g0 = cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e0.off));
+        const Tacc g1 = cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e1.off));
         a = fma(e0.val, g0, a);
         a = fma(e1.val, g1, a);
       }
       if (e < end) {
         const Ent e0 = E[e];
-        a = fma(e0.val, cvt<Tacc>(t[e0.off]), a);
+        a = fma(e0.val, cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e0.off)), a);
         ++e;
       }
       acc[b] = a;
@@ -193,7 +194,7 @@ void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
   for (size_t i = 0; i < jobs.size(); ++i) {
     const S1Job& J = jobs[i];
     require(J.pr->p->r == r, "compress group: projectors must share r");
-    const ChunkTable& ct = J.pr->p->chunk_table(bm);
+    const ChunkTable& ct = J.pr->p->chunk_table(bm, static_cast<int>(sizeof(Tin)));
     S1Mat& M = A.mat[i];
     M.g = J.g, M.ldg = J.ldg, M.m = J.pr->m, M.n = J.pr->n;
     M.split = ct.split.as<int>(), M.ent = ct.ent.p, M.nchunks = ct.nchunks;

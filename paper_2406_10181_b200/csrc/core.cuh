@@ -35,8 +35,9 @@ struct DevBuf {
   }
 };
 
-// Entry of the chunk-major stage-1 table: tile offset (row_in_chunk * 32) and value.
-struct EntryF {
+// Entry of the chunk-major stage-1 table: byte offset of the entry's row in
+// the shared-memory G tile (row_in_chunk * 32 * sizeof(Tin)) and value.
+struct __align__(8) EntryF {
   int32_t off;
   float val;
 };
@@ -58,6 +59,7 @@ struct EntryOf<double> {
 
 struct ChunkTable {
   int bm = 0;
+  int esize = 0;  // sizeof(Tin) the byte offsets were scaled for
   int nchunks = 0;
   DevBuf split;  // int32 [nchunks*d + 1]
   DevBuf ent;    // EntryF / EntryD [nnz]
@@ -78,7 +80,7 @@ struct Projector {
 
   size_t nnz() const { return static_cast<size_t>(n_rows) * r; }
   size_t vsize() const { return dtype_size(compute); }
-  const ChunkTable& chunk_table(int bm);
+  const ChunkTable& chunk_table(int bm, int esize);
   // Re-derive CSC and chunk-table values from the CSR values on the device.
   void refresh_values(cudaStream_t st);
   void upload_values();  // h_val -> device CSR values, then refresh
@@ -152,6 +154,9 @@ void launch_transpose(int rows, int cols, const void* src, long long lds, void* 
 void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long long ldi,
                        void* out, long long ldo, lsp_dtype dt, double alpha, double beta,
                        const int* skip_flag, DevBuf* partials, int* nparts, cudaStream_t st);
+// TMA/mbarrier fast path; returns false when the shapes or pointers do not allow it.
+bool launch_decompress_group_tma(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
+                                 double beta, const int* skip_flag, cudaStream_t st);
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st);

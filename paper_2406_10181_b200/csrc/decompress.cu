@@ -17,6 +17,7 @@
 //     read-modify-write of W[i][band].  W is read and written exactly once.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "core.cuh"
@@ -339,6 +340,12 @@ void decompress_impl(const std::vector<DecJob>& jobs, double alpha, double beta,
 
 }  // namespace
 
+// LSP_DECOMPRESS_GENERIC=1 forces the cp.async kernel (tests cover both paths).
+static bool force_generic() {
+  const char* e = std::getenv("LSP_DECOMPRESS_GENERIC");
+  return e && e[0] == '1';
+}
+
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st) {
@@ -349,6 +356,9 @@ void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, doub
   for (const DecJob& J : jobs)
     require(J.pr->d == p0.d && J.pr->p->r == p0.p->r && J.pr->compute == p0.compute,
             "decompress group: matrices must share d, r and compute dtype");
+  if (!partials && !force_generic() &&
+      launch_decompress_group_tma(jobs, dt, alpha, beta, skip_flag, st))
+    return;
   LSP_DISPATCH_ACC(p0.compute, Tacc, {
     LSP_DISPATCH_STORAGE(dt, Tw, {
       constexpr int kBudget = 220 * 1024;

@@ -320,3 +320,20 @@ def test_launch_count_increases(cuda, port):
     before = lsp.launch_count()
     pair.compress(torch.randn(64, 64, device="cuda"))
     assert lsp.launch_count() >= before + 2
+
+
+@pytest.mark.parametrize("generic", ["0", "1"])
+def test_decompress_paths_agree(cuda, port, generic, monkeypatch):
+    """The TMA/mbarrier kernel and the generic cp.async kernel are bitwise identical
+    and both match the oracle (incl. ragged m, n and the group tile split)."""
+    monkeypatch.setenv("LSP_DECOMPRESS_GENERIC", generic)
+    for (m, n, d) in [(777, 1000, 64), (130, 4100, 128), (4096, 96, 256)]:
+        P, Q, pair = make(port, m, n, d, 4, m + n)
+        delta = f32normal(d, (d, d))
+        w0 = f32normal(n, (m, n), 0.02)
+        w = dev(w0)
+        pair.decompress_apply(dev(delta), 1e-3, w)
+        ref = port.decompress_apply(P, Q, delta, 1e-3, w0)
+        assert rel(host(w) - w0, ref - w0) < 1e-5
+        out = host(pair.decompress(dev(delta)))
+        assert rel(out, port.decompress(P, Q, delta)) < 1e-5
