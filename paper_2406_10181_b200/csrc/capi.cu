@@ -87,13 +87,14 @@ const ChunkTable& Projector::chunk_table(int bm, int esize) {
   build_chunks(n_rows, d, bm, h_csc_ptr, h_csc_rows, h_csc_perm, split, rows, perm);
   upload(ct->split, split.data(), split.size() * sizeof(int32_t));
   upload(ct->perm, perm.data(), perm.size() * sizeof(int32_t));
+  ct->count = static_cast<long long>(perm.size());
   LSP_DISPATCH_ACC(compute, T, {
     using E = typename EntryOf<T>::type;
     std::vector<E> ent(rows.size());
     for (size_t t = 0; t < rows.size(); ++t) {
       ent[t] = E{};
       ent[t].off = rows[t] * 32 * esize;
-      ent[t].val = static_cast<T>(h_val[perm[t]]);
+      ent[t].val = perm[t] >= 0 ? static_cast<T>(h_val[perm[t]]) : T(0);
     }
     upload(ct->ent, ent.data(), ent.size() * sizeof(E));
   })

@@ -13,6 +13,7 @@
 //  stage 2  S^T[b][:] = sum_{j in CSC_Q(b)} q_jb Z^T[j][:]  -- coalesced row
 //           gathers of the L2-resident Z^T (k_gather).
 #include <algorithm>
+#include <type_traits>
 
 #include "core.cuh"
 
@@ -24,6 +25,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
                "r"(src_bytes));
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -108,12 +112,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
   auto stage = [&](int c, int buf) {
     unsigned char* base = smem_raw + buf * stage_bytes;
     load_tile<Tin, NT>(reinterpret_cast<Tin*>(base), g, M.ldg, m, n, c * bm, j0, bm, vec16);
-    // the chunk's entries: [c*bm*r, c*bm*r + rows*r), contiguous in the table
-    const long long e0 = static_cast<long long>(c) * bm * r;
-    const int bytes = min(bm, m - c * bm) * r * static_cast<int>(sizeof(Ent));
+    // the chunk's (even-padded) entries are contiguous in the table
+    const int e0 = __ldg(split + static_cast<long long>(c) * d);
+    const int e1 = __ldg(split + static_cast<long long>(c + 1) * d);
+    const int bytes = (e1 - e0) * static_cast<int>(sizeof(Ent));
     const char* src = reinterpret_cast<const char*>(ent + e0);
     char* dst = reinterpret_cast<char*>(base + A.tile_bytes);
-    for (int p = threadIdx.x * 16; p < bytes; p += NT * 16) cp_async16(dst + p, src + p, min(16, bytes - p));
+    for (int p = threadIdx.x * 16; p < bytes; p += NT * 16)
+      cp_async16(dst + p, src + p, min(16, bytes - p));
   };
 
   Tacc acc[32];
@@ -131,31 +137,60 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
     cp_async_commit();
     const unsigned char* base = smem_raw + (c & 1) * stage_bytes;
     const unsigned char* tb = base + lane * sizeof(Tin);  // + entry byte offset = G[row][lane]
-    const Ent* E = reinterpret_cast<const Ent*>(base + A.tile_bytes) -
-                   static_cast<long long>(c) * bm * r;  // indexed by global entry id
-    // Entries of (chunk c, bin) are contiguous and bins follow each other, so
-    // bin b's range is [end(b-1), end(b)).
+    // Entries of (chunk c, bin) are contiguous, even-padded, and bins follow
+    // each other, so bin b's range is [end(b-1), end(b)).
     const long long sbase = static_cast<long long>(c) * d;
+    const int cbeg = __ldg(split + sbase);
+    const Ent* E = reinterpret_cast<const Ent*>(base + A.tile_bytes) - cbeg;
     int e = __ldg(split + sbase + min(bin0, d));
     const int my_end = __ldg(split + sbase + min(my_bin + 1, d));
+    if constexpr (std::is_same<Tin, float>::value && std::is_same<Tacc, float>::value) {
+      // Two entries per 16-byte load; bra.uni keeps the warp-uniform loop free
+      // of divergence bookkeeping.
+      const unsigned e_base = smem_u32(base + A.tile_bytes) - static_cast<unsigned>(cbeg) * 8u;
+      const unsigned t_lane = smem_u32(tb);
+      unsigned ep = e_base + static_cast<unsigned>(e) * 8u;
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      const int end = __shfl_sync(0xffffffffu, my_end, b);
-      Tacc a = acc[b];
+      for (int b = 0; b < 32; ++b) {
+        const unsigned ep_end = e_base + static_cast<unsigned>(__shfl_sync(0xffffffffu, my_end, b)) * 8u;
+        float a = acc[b];
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 o0, o1, w0, w1;\n\t.reg .f32 v0, v1, g0, g1;\n"
+            "LSPS1_L%=:\n\t"
+            "setp.ge.u32 p, %1, %2;\n\t"
+            "@p bra.uni LSPS1_E%=;\n\t"
+            "ld.shared.v4.b32 {o0, w0, o1, w1}, [%1];\n\t"
+            "add.u32 o0, o0, %3;\n\t"
+            "add.u32 o1, o1, %3;\n\t"
+            "mov.b32 v0, w0;\n\t"
+            "mov.b32 v1, w1;\n\t"
+            "ld.shared.f32 g0, [o0];\n\t"
+            "ld.shared.f32 g1, [o1];\n\t"
+            "fma.rn.f32 %0, v0, g0, %0;\n\t"
+            "fma.rn.f32 %0, v1, g1, %0;\n\t"
+            "add.u32 %1, %1, 16;\n\t"
+            "bra.uni LSPS1_L%=;\n"
+            "LSPS1_E%=:\n\t}"
+            : "+f"(a), "+r"(ep)
+            : "r"(ep_end), "r"(t_lane)
+            : "memory");
+        acc[b] = a;
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        const int end = __shfl_sync(0xffffffffu, my_end, b);
+        Tacc a = acc[b];
 #pragma unroll 1
-      for (; e + 1 < end; e += 2) {
-        const Ent e0 = E[e], e1 = E[e + 1];
-        const Tacc g0 = cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e0.off));
-        const Tacc g1 = cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e1.off));
-        a = fma(e0.val, g0, a);
-        a = fma(e1.val, g1, a);
+        for (; e < end; e += 2) {  // segments are even-padded
+          const Ent e0 = E[e], e1 = E[e + 1];
+          const Tacc g0 = cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e0.off));
+          const Tacc g1 = cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e1.off));
+          a = fma(e0.val, g0, a);
+          a = fma(e1.val, g1, a);
+        }
+        acc[b] = a;
       }
-      if (e < end) {
-        const Ent e0 = E[e];
-        a = fma(e0.val, cvt<Tacc>(*reinterpret_cast<const Tin*>(tb + e0.off)), a);
-        ++e;
-      }
-      acc[b] = a;
     }
   }
   const int j = j0 + lane;
@@ -180,7 +215,7 @@ void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
   const int r = jobs[0].pr->p->r;
   // Per-stage budget: ~100 KB (two stages fit the 227 KB of an SM) for the
   // 32-warp kernel, half that for smaller CTAs so several fit per SM.
-  const int budget = WARPS >= 16 ? 100 * 1024 : 48 * 1024;
+  const int budget = (WARPS >= 16 ? 100 * 1024 : 48 * 1024) - d * static_cast<int>(sizeof(Ent));
   const int row_bytes = 32 * static_cast<int>(sizeof(Tin)) + r * static_cast<int>(sizeof(Ent));
   const int bm = std::max(32, (budget / row_bytes) / 32 * 32);
   S1Args A{};
@@ -189,7 +224,8 @@ void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
   A.r = r;
   A.bm = bm;
   A.tile_bytes = static_cast<int>(round_up(static_cast<long long>(bm) * 32 * sizeof(Tin), 16));
-  A.ent_bytes = static_cast<int>(round_up(static_cast<long long>(bm) * r * sizeof(Ent), 16));
+  // a chunk holds bm*r entries plus at most one even-padding entry per bin
+  A.ent_bytes = static_cast<int>(round_up(static_cast<long long>(bm * r + d) * sizeof(Ent), 16));
   int bands = 0;
   for (size_t i = 0; i < jobs.size(); ++i) {
     const S1Job& J = jobs[i];

@@ -61,9 +61,10 @@ struct ChunkTable {
   int bm = 0;
   int esize = 0;  // sizeof(Tin) the byte offsets were scaled for
   int nchunks = 0;
+  long long count = 0;  // entries incl. even-length padding
   DevBuf split;  // int32 [nchunks*d + 1]
   DevBuf ent;    // EntryF / EntryD [nnz]
-  DevBuf perm;   // int32 [nnz] -> CSR index (for value refresh)
+  DevBuf perm;   // int32 [count] -> CSR index (-1 for padding), for value refresh
 };
 
 // Device-resident SparseProjector (proj/include/lsp/projector.hpp:18-30) in

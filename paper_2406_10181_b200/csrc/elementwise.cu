@@ -124,7 +124,7 @@ __global__ void k_gather_entry_values(long long cnt, const int* __restrict__ per
                                       const T* __restrict__ src, E* __restrict__ dst) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
        i += (long long)gridDim.x * blockDim.x)
-    dst[i].val = src[perm[i]];
+    if (perm[i] >= 0) dst[i].val = src[perm[i]];
 }
 
 int grid_for(long long cnt) {
@@ -224,7 +224,7 @@ void launch_refresh_values(const Projector& p, cudaStream_t st) {
     after_launch("refresh_csc");
     for (const auto& ct : p.chunks) {
       using E = typename EntryOf<T>::type;
-      k_gather_entry_values<E, T><<<grid_for(nnz), 256, 0, st>>>(nnz, ct->perm.as<int>(),
+      k_gather_entry_values<E, T><<<grid_for(ct->count), 256, 0, st>>>(ct->count, ct->perm.as<int>(),
                                                                  p.val.as<T>(), ct->ent.as<E>());
       after_launch("refresh_chunks");
     }

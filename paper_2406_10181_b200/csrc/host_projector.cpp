@@ -185,7 +185,10 @@ void build_csc(int n_rows, int d, int r, const int32_t* pos, std::vector<int32_t
 
 // Chunk-major entry table for the compress stage-1 kernel: entries ordered by
 // (row chunk of `bm` rows, column, row).  split[c*d + a] is the first entry of
-// (chunk c, column a); split[nchunks*d] = nnz.  row_in_chunk = row - c*bm.
+// (chunk c, column a); split[nchunks*d] = total.  row_in_chunk = row - c*bm.
+// Every (chunk, column) segment is padded to an EVEN length with a dummy
+// entry (row 0 of the chunk, value 0, perm -1) so the kernel consumes two
+// entries per 16-byte shared-memory load with no remainder branch.
 void build_chunks(int n_rows, int d, int bm, const std::vector<int32_t>& csc_ptr,
                   const std::vector<int32_t>& csc_rows, const std::vector<int32_t>& csc_perm,
                   std::vector<int32_t>& split, std::vector<int32_t>& row_in_chunk,
@@ -193,25 +196,31 @@ void build_chunks(int n_rows, int d, int bm, const std::vector<int32_t>& csc_ptr
   const int nchunks = ceil_div(n_rows, bm);
   const size_t nnz = csc_rows.size();
   split.assign(static_cast<size_t>(nchunks) * d + 1, 0);
-  row_in_chunk.resize(nnz);
-  perm.resize(nnz);
+  row_in_chunk.clear();
+  perm.clear();
+  row_in_chunk.reserve(nnz + nnz / 4 + d);
+  perm.reserve(nnz + nnz / 4 + d);
   // cursor[a] walks column a's (row-sorted) entries chunk by chunk
   std::vector<int32_t> cursor(csc_ptr.begin(), csc_ptr.end() - 1);
-  size_t t = 0;
   for (int c = 0; c < nchunks; ++c) {
     const int lim = (c + 1) * bm;
     for (int a = 0; a < d; ++a) {
-      split[static_cast<size_t>(c) * d + a] = static_cast<int32_t>(t);
+      split[static_cast<size_t>(c) * d + a] = static_cast<int32_t>(perm.size());
       int32_t& cu = cursor[a];
+      int cnt = 0;
       while (cu < csc_ptr[a + 1] && csc_rows[cu] < lim) {
-        row_in_chunk[t] = csc_rows[cu] - c * bm;
-        perm[t] = csc_perm[cu];
-        ++t;
+        row_in_chunk.push_back(csc_rows[cu] - c * bm);
+        perm.push_back(csc_perm[cu]);
         ++cu;
+        ++cnt;
+      }
+      if (cnt & 1) {  // pad to even
+        row_in_chunk.push_back(0);
+        perm.push_back(-1);
       }
     }
   }
-  split[static_cast<size_t>(nchunks) * d] = static_cast<int32_t>(t);
+  split[static_cast<size_t>(nchunks) * d] = static_cast<int32_t>(perm.size());
 }
 
 }  // namespace lspb
