@@ -102,6 +102,17 @@ const ChunkTable& Projector::chunk_table(int bm, int esize) {
   return *chunks.back();
 }
 
+const int* Projector::scaled_pos(int scale) {
+  for (auto& e : scaled)
+    if (e.first == scale) return e.second->as<int>();
+  std::vector<int32_t> sp(h_pos.size());
+  for (size_t i = 0; i < sp.size(); ++i) sp[i] = h_pos[i] * scale;
+  auto buf = std::make_unique<DevBuf>();
+  upload(*buf, sp.data(), sp.size() * sizeof(int32_t));
+  scaled.emplace_back(scale, std::move(buf));
+  return scaled.back().second->as<int>();
+}
+
 int* Pair::flag_ptr() {
   if (!flag.p) {
     flag.ensure(sizeof(int));

@@ -150,29 +150,34 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
       const unsigned e_base = smem_u32(base + A.tile_bytes) - static_cast<unsigned>(cbeg) * 8u;
       const unsigned t_lane = smem_u32(tb);
       unsigned ep = e_base + static_cast<unsigned>(e) * 8u;
+      // software pipeline: the current pair {o0, v0, o1, v1} is always preloaded
+      // (the stage has 16 bytes of slack, so preloading past the end is safe)
+      unsigned o0, w0, o1, w1;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(o0), "=r"(w0), "=r"(o1), "=r"(w1) : "r"(ep));
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
         const unsigned ep_end = e_base + static_cast<unsigned>(__shfl_sync(0xffffffffu, my_end, b)) * 8u;
         float a = acc[b];
         asm volatile(
-            "{\n\t.reg .pred p;\n\t.reg .b32 o0, o1, w0, w1;\n\t.reg .f32 v0, v1, g0, g1;\n"
+            "{\n\t.reg .pred p;\n\t.reg .b32 a0, a1;\n\t.reg .f32 v0, v1, g0, g1;\n"
             "LSPS1_L%=:\n\t"
             "setp.ge.u32 p, %1, %2;\n\t"
             "@p bra.uni LSPS1_E%=;\n\t"
-            "ld.shared.v4.b32 {o0, w0, o1, w1}, [%1];\n\t"
-            "add.u32 o0, o0, %3;\n\t"
-            "add.u32 o1, o1, %3;\n\t"
-            "mov.b32 v0, w0;\n\t"
-            "mov.b32 v1, w1;\n\t"
-            "ld.shared.f32 g0, [o0];\n\t"
-            "ld.shared.f32 g1, [o1];\n\t"
+            "add.u32 a0, %3, %7;\n\t"
+            "add.u32 a1, %5, %7;\n\t"
+            "mov.b32 v0, %4;\n\t"
+            "mov.b32 v1, %6;\n\t"
+            "ld.shared.f32 g0, [a0];\n\t"
+            "ld.shared.f32 g1, [a1];\n\t"
+            "add.u32 %1, %1, 16;\n\t"
+            "ld.shared.v4.b32 {%3, %4, %5, %6}, [%1];\n\t"
             "fma.rn.f32 %0, v0, g0, %0;\n\t"
             "fma.rn.f32 %0, v1, g1, %0;\n\t"
-            "add.u32 %1, %1, 16;\n\t"
             "bra.uni LSPS1_L%=;\n"
             "LSPS1_E%=:\n\t}"
-            : "+f"(a), "+r"(ep)
-            : "r"(ep_end), "r"(t_lane)
+            : "+f"(a), "+r"(ep), "+r"(ep_end), "+r"(o0), "+r"(w0), "+r"(o1), "+r"(w1)
+            : "r"(t_lane)
             : "memory");
         acc[b] = a;
       }
@@ -225,7 +230,7 @@ void stage1_impl(const std::vector<S1Job>& jobs, int d, cudaStream_t st) {
   A.bm = bm;
   A.tile_bytes = static_cast<int>(round_up(static_cast<long long>(bm) * 32 * sizeof(Tin), 16));
   // a chunk holds bm*r entries plus at most one even-padding entry per bin
-  A.ent_bytes = static_cast<int>(round_up(static_cast<long long>(bm * r + d) * sizeof(Ent), 16));
+  A.ent_bytes = static_cast<int>(round_up(static_cast<long long>(bm * r + d) * sizeof(Ent), 16) + 16);
   int bands = 0;
   for (size_t i = 0; i < jobs.size(); ++i) {
     const S1Job& J = jobs[i];

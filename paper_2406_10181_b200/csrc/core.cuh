@@ -82,6 +82,10 @@ struct Projector {
   size_t nnz() const { return static_cast<size_t>(n_rows) * r; }
   size_t vsize() const { return dtype_size(compute); }
   const ChunkTable& chunk_table(int bm, int esize);
+  // CSR positions multiplied by `scale` (cached per scale), for kernels that
+  // index shared-memory rows by byte offset.
+  const int* scaled_pos(int scale);
+  std::vector<std::pair<int, std::unique_ptr<DevBuf>>> scaled;
   // Re-derive CSC and chunk-table values from the CSR values on the device.
   void refresh_values(cudaStream_t st);
   void upload_values();  // h_val -> device CSR values, then refresh

@@ -68,7 +68,7 @@ constexpr int kKR = 4;        // nonzeros per projector row handled by this path
 struct alignas(64) TMat {
   CUtensorMap tmap;  // W (input) tile map: box BN x kTRows
   int m, n;
-  const int* ppos;
+  const int* ppos_scaled;  // P positions * (BN+1) * sizeof(Tacc): Y_band row byte offsets
   const void* pval;
   const int* qpos;
   const void* qval;
@@ -85,6 +85,17 @@ struct TArgs {
   double alpha, beta;
   const int* skip;
 };
+
+__device__ __forceinline__ float lds_f(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double lds_d(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
 
 struct TCursor {
   int mi, band, rb;
@@ -160,7 +171,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_decompress_tma(const __grid_co
         const unsigned pbytes = nrows * kKR * 4, vbytes = nrows * kKR * sizeof(Tacc);
         mbar_arrive_expect_tx(full + st, (USE_IN ? L.w_bytes() : 0) + pbytes + vbytes);
         if (USE_IN) tma_load_2d(base, &M.tmap, c.band * BN, r0, full + st, pol);
-        bulk_load(base + L.w_bytes(), M.ppos + static_cast<long long>(r0) * kKR, pbytes, full + st);
+        bulk_load(base + L.w_bytes(), M.ppos_scaled + static_cast<long long>(r0) * kKR, pbytes,
+                  full + st);
         bulk_load(base + L.w_bytes() + L.pos_bytes(),
                   static_cast<const Tacc*>(M.pval) + static_cast<long long>(r0) * kKR, vbytes,
                   full + st);
@@ -204,7 +216,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_decompress_tma(const __grid_co
   constexpr int RPW = 32 / BN;                    // rows per warp instruction
   constexpr int kIters = kTRows / (kConsumers * RPW);
   const int jj = lane % BN, rsub = lane / BN;
-  const Tacc* ycol = Y + jj;
+  // byte address of Y_band[0][jj]; rows of Y_band are LDY*sizeof(Tacc) bytes apart
+  const unsigned y_lane = smem_addr(Y) + jj * static_cast<unsigned>(sizeof(Tacc));
   TCursor c = tcursor_at(A, t_begin);
   int cur_band = -1, cur_mat = -1;
   for (int s = 0; s < ntiles; ++s, tadvance(A, c)) {
@@ -217,37 +230,49 @@ __global__ void __launch_bounds__(kTThreads, 1) k_decompress_tma(const __grid_co
       cur_mat = c.mi;
     }
     const int st = s % kTStages;
-    mbar_wait(full + st, (s / kTStages) & 1);
-    const unsigned char* base = ring + st * L.stage_bytes();
-    const Tw* wt = reinterpret_cast<const Tw*>(base);
-    const int* ps = reinterpret_cast<const int*>(base + L.w_bytes());
-    const Tacc* vs = reinterpret_cast<const Tacc*>(base + L.w_bytes() + L.pos_bytes());
     const int r0 = c.rb * kTRows;
     const int nrows = min(kTRows, M.m - r0);
     const int j = c.band * BN + jj;
-    if (j < M.n) {
-      Tw* orow = static_cast<Tw*>(M.out) + static_cast<long long>(r0) * M.ldo + j;
+    const long long ldo = M.ldo;
+    Tw* const out = static_cast<Tw*>(M.out);
+    const bool col_ok = j < M.n;
+    mbar_wait(full + st, (s / kTStages) & 1);
+    const unsigned char* base = ring + st * L.stage_bytes();
+    const Tw* wt = reinterpret_cast<const Tw*>(base);
+    // P entries of the tile, already scaled to Y_band row byte offsets
+    const int* ps = reinterpret_cast<const int*>(base + L.w_bytes());
+    const Tacc* vs = reinterpret_cast<const Tacc*>(base + L.w_bytes() + L.pos_bytes());
+    if (col_ok) {
+      const int q0 = warp * RPW + rsub;
+      Tw* orow = out + static_cast<long long>(r0 + q0) * ldo + j;
+      const long long ostep = static_cast<long long>(kConsumers * RPW) * ldo;
+      auto row = [&](int q, Tw* o) {
+        const int4 pp = *reinterpret_cast<const int4*>(ps + q * kKR);
+        Tacc acc;
+        if constexpr (sizeof(Tacc) == 4) {
+          const float4 vv = *reinterpret_cast<const float4*>(vs + q * kKR);
+          acc = vv.x * lds_f(y_lane + pp.x);
+          acc = fma(vv.y, lds_f(y_lane + pp.y), acc);
+          acc = fma(vv.z, lds_f(y_lane + pp.z), acc);
+          acc = fma(vv.w, lds_f(y_lane + pp.w), acc);
+        } else {
+          acc = vs[q * kKR] * lds_d(y_lane + pp.x);
+          acc = fma(vs[q * kKR + 1], lds_d(y_lane + pp.y), acc);
+          acc = fma(vs[q * kKR + 2], lds_d(y_lane + pp.z), acc);
+          acc = fma(vs[q * kKR + 3], lds_d(y_lane + pp.w), acc);
+        }
+        Tacc res = alpha * acc;
+        if (USE_IN) res = fma(beta, cvt<Tacc>(wt[q * BN + jj]), res);
+        *o = cvt<Tw>(res);
+      };
+      if (nrows == kTRows) {
 #pragma unroll
-      for (int u = 0; u < kIters; ++u) {
-        const int q = (u * kConsumers + warp) * RPW + rsub;
-        if (q < nrows) {
-          const int4 pp = *reinterpret_cast<const int4*>(ps + q * kKR);
-          Tacc acc;
-          if constexpr (sizeof(Tacc) == 4) {
-            const float4 vv = *reinterpret_cast<const float4*>(vs + q * kKR);
-            acc = vv.x * ycol[pp.x * LDY];
-            acc = fma(vv.y, ycol[pp.y * LDY], acc);
-            acc = fma(vv.z, ycol[pp.z * LDY], acc);
-            acc = fma(vv.w, ycol[pp.w * LDY], acc);
-          } else {
-            acc = vs[q * kKR] * ycol[pp.x * LDY];
-            acc = fma(vs[q * kKR + 1], ycol[pp.y * LDY], acc);
-            acc = fma(vs[q * kKR + 2], ycol[pp.z * LDY], acc);
-            acc = fma(vs[q * kKR + 3], ycol[pp.w * LDY], acc);
-          }
-          Tacc res = alpha * acc;
-          if (USE_IN) res = fma(beta, cvt<Tacc>(wt[q * BN + jj]), res);
-          orow[static_cast<long long>(q) * M.ldo] = cvt<Tw>(res);
+        for (int u = 0; u < kIters; ++u) row(q0 + u * kConsumers * RPW, orow + u * ostep);
+      } else {
+#pragma unroll 1
+        for (int u = 0; u < kIters; ++u) {
+          const int q = q0 + u * kConsumers * RPW;
+          if (q < nrows) row(q, orow + u * ostep);
         }
       }
     }
@@ -301,8 +326,7 @@ bool tma_impl(const std::vector<DecJob>& jobs, double alpha, double beta, const 
     const Pair& pr = *J.pr;
     if (pr.p->r != kKR || pr.q->r != kKR) return false;
     if (use_in && J.in == nullptr) return false;
-    if (reinterpret_cast<uintptr_t>(pr.p->pos.p) % 16 || reinterpret_cast<uintptr_t>(pr.p->val.p) % 16)
-      return false;
+    if (reinterpret_cast<uintptr_t>(pr.p->val.p) % 16) return false;
     TMat& M = A.mat[i];
     if (use_in && !cached_tmap(&M.tmap, J.in, std::is_same<Tw, double>::value  ? LSP_F64
                                               : std::is_same<Tw, float>::value ? LSP_F32
@@ -310,7 +334,8 @@ bool tma_impl(const std::vector<DecJob>& jobs, double alpha, double beta, const 
                                pr.m, pr.n, J.ldi, BN, kTRows))
       return false;
     M.m = pr.m, M.n = pr.n;
-    M.ppos = pr.p->pos.as<int>(), M.pval = pr.p->val.p;
+    M.ppos_scaled = pr.p->scaled_pos((BN + 1) * static_cast<int>(sizeof(Tacc)));
+    M.pval = pr.p->val.p;
     M.qpos = pr.q->pos.as<int>(), M.qval = pr.q->val.p;
     M.dT = J.delta_t;
     M.out = J.out, M.ldo = J.ldo;
