@@ -102,6 +102,47 @@ const ChunkTable& Projector::chunk_table(int bm, int esize) {
   return *chunks.back();
 }
 
+const SlotTable& Projector::slot_table(int bm, int row_bytes, int K, int bpw) {
+  for (auto& t : slot_tables)
+    if (t->bm == bm && t->row_bytes == row_bytes && t->K == K && t->bpw == bpw) return *t;
+  require(K >= 2 && K % 2 == 0 && bpw >= 1 && 32 % bpw == 0, "slot table: bad K / bins per warp");
+  auto t = std::make_unique<SlotTable>();
+  t->bm = bm, t->row_bytes = row_bytes, t->K = K, t->bpw = bpw;
+  t->nchunks = ceil_div(n_rows, bm);
+  t->dpad = static_cast<int>(round_up(d, 32));
+  SlotHost h;
+  build_slots(n_rows, d, bm, K, bpw, h_csc_ptr, h_csc_rows, h_csc_perm, h);
+  t->nslots = static_cast<long long>(h.slot_row.size());
+  t->novf = static_cast<long long>(h.ovf_row.size());
+  const int zero = slot_zero_off(bm, row_bytes);
+  require(static_cast<long long>(zero) < (1LL << 27), "slot table: tile too large");
+  std::vector<EntryF> sl(h.slot_row.size()), ov(h.ovf_row.size());
+  for (size_t i = 0; i < sl.size(); ++i) {
+    const int row = h.slot_row[i];
+    sl[i].off = row < 0 ? zero : row * row_bytes;
+    sl[i].val = row < 0 ? 0.0f : static_cast<float>(h_val[h.slot_perm[i]]);
+  }
+  for (size_t i = 0; i < ov.size(); ++i) {
+    ov[i].off = (h.ovf_row[i] * row_bytes) | (h.ovf_bin[i] << 27);
+    ov[i].val = static_cast<float>(h_val[h.ovf_perm[i]]);
+  }
+  upload(t->slots, sl.data(), sl.size() * sizeof(EntryF));
+  upload(t->perm, h.slot_perm.data(), h.slot_perm.size() * sizeof(int32_t));
+  upload(t->ovf_split, h.ovf_split.data(), h.ovf_split.size() * sizeof(int32_t));
+  upload(t->ovf, ov.data(), ov.size() * sizeof(EntryF));
+  upload(t->ovf_perm, h.ovf_perm.data(), h.ovf_perm.size() * sizeof(int32_t));
+  slot_tables.push_back(std::move(t));
+  return *slot_tables.back();
+}
+
+long long Projector::overflow(int K, int bm) {
+  for (auto& e : ovf_counts)
+    if (e.first == std::make_pair(K, bm)) return e.second;
+  const long long v = count_overflow(n_rows, d, bm, K, h_csc_ptr, h_csc_rows);
+  ovf_counts.emplace_back(std::make_pair(K, bm), v);
+  return v;
+}
+
 const int* Projector::scaled_pos(int scale) {
   for (auto& e : scaled)
     if (e.first == scale) return e.second->as<int>();

@@ -67,6 +67,23 @@ struct ChunkTable {
   DevBuf perm;   // int32 [count] -> CSR index (-1 for padding), for value refresh
 };
 
+// Fixed-slot stage-1 table (see build_slots): K slots per (chunk, bin), an
+// overflow list per (chunk, 32-bin group).  Padding slots point at the zero
+// row that follows the bm-row G tile in shared memory.
+struct SlotTable {
+  int bm = 0, row_bytes = 0, K = 0, bpw = 0, nchunks = 0, dpad = 0;
+  long long nslots = 0, novf = 0;
+  DevBuf slots;      // EntryF [nchunks][dpad][K]: off = tile byte offset, val
+  DevBuf perm;       // int32 [nslots] -> CSR index (-1: padding)
+  DevBuf ovf_split;  // int32 [nchunks*dpad/bpw + 1]
+  DevBuf ovf;        // EntryF [novf]: off | (bin % bpw) << 27, val
+  DevBuf ovf_perm;   // int32 [novf]
+};
+// Byte offset of the zero row (= bytes of a bm-row tile, 128-aligned).
+inline int slot_zero_off(int bm, int row_bytes) {
+  return static_cast<int>(round_up(static_cast<long long>(bm) * row_bytes, 128));
+}
+
 // Device-resident SparseProjector (proj/include/lsp/projector.hpp:18-30) in
 // CSR (row-major positions/values, the reference layout) and CSC orientation.
 struct Projector {
@@ -78,10 +95,14 @@ struct Projector {
   DevBuf pos, val;                           // CSR: int32 / compute [n_rows*r]
   DevBuf csc_ptr, csc_row, csc_val, csc_perm;  // CSC: [d+1], [nnz], [nnz], [nnz]
   std::vector<std::unique_ptr<ChunkTable>> chunks;
+  std::vector<std::unique_ptr<SlotTable>> slot_tables;
+  std::vector<std::pair<std::pair<int, int>, long long>> ovf_counts;  // (K, bm) -> overflow
 
   size_t nnz() const { return static_cast<size_t>(n_rows) * r; }
   size_t vsize() const { return dtype_size(compute); }
   const ChunkTable& chunk_table(int bm, int esize);
+  const SlotTable& slot_table(int bm, int row_bytes, int K, int bpw);
+  long long overflow(int K, int bm);
   // CSR positions multiplied by `scale` (cached per scale), for kernels that
   // index shared-memory rows by byte offset.
   const int* scaled_pos(int scale);
@@ -144,6 +165,8 @@ void launch_compress_stage1(const Pair& pr, const void* g, long long ldg, lsp_dt
                             void* zt, cudaStream_t st);
 void launch_compress_stage1_group(const std::vector<S1Job>& jobs, lsp_dtype gdt,
                                   cudaStream_t st);
+// Fixed-slot TMA variant (compress_slots.cu); false if the group is not eligible.
+bool launch_compress_slots_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, cudaStream_t st);
 void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t st);
 void compress_group_T(const std::vector<S1Job>& jobs, lsp_dtype gdt, int* flag,
                       cudaStream_t st);

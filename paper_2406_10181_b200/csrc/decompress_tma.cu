@@ -58,6 +58,35 @@ bool encode_tmap_2d(CUtensorMap* map, const void* base, lsp_dtype dt, long long 
 }
 
 namespace {
+struct MapKey {
+  const void* p;
+  long long rows, cols, ld;
+  int dt, bc, br;
+  bool operator<(const MapKey& o) const {
+    return std::tie(p, rows, cols, ld, dt, bc, br) < std::tie(o.p, o.rows, o.cols, o.ld, o.dt, o.bc, o.br);
+  }
+};
+
+}  // namespace
+
+bool cached_tmap(CUtensorMap* out, const void* base, lsp_dtype dt, long long rows, long long cols,
+                 long long ld, int bc, int br) {
+  static std::mutex mu;
+  static std::map<MapKey, CUtensorMap> cache;
+  const MapKey k{base, rows, cols, ld, static_cast<int>(dt), bc, br};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(k);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (!encode_tmap_2d(out, base, dt, rows, cols, ld, bc, br)) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(k, *out);
+  return true;
+}
+
+namespace {
 
 constexpr int kTRows = 128;   // W rows per stage
 constexpr int kTStages = 4;   // ring depth
@@ -279,32 +308,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_decompress_tma(const __grid_co
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
   }
-}
-
-struct MapKey {
-  const void* p;
-  long long rows, cols, ld;
-  int dt, bc, br;
-  bool operator<(const MapKey& o) const {
-    return std::tie(p, rows, cols, ld, dt, bc, br) < std::tie(o.p, o.rows, o.cols, o.ld, o.dt, o.bc, o.br);
-  }
-};
-
-bool cached_tmap(CUtensorMap* out, const void* base, lsp_dtype dt, long long rows, long long cols,
-                 long long ld, int bc, int br) {
-  static std::mutex mu;
-  static std::map<MapKey, CUtensorMap> cache;
-  const MapKey k{base, rows, cols, ld, static_cast<int>(dt), bc, br};
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(k);
-  if (it != cache.end()) {
-    *out = it->second;
-    return true;
-  }
-  if (!encode_tmap_2d(out, base, dt, rows, cols, ld, bc, br)) return false;
-  if (cache.size() > 4096) cache.clear();
-  cache.emplace(k, *out);
-  return true;
 }
 
 template <typename Tw, typename Tacc, int BN>

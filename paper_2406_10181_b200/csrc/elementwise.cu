@@ -228,6 +228,18 @@ void launch_refresh_values(const Projector& p, cudaStream_t st) {
                                                                  p.val.as<T>(), ct->ent.as<E>());
       after_launch("refresh_chunks");
     }
+    if constexpr (sizeof(T) == 4) {
+      for (const auto& t : p.slot_tables) {
+        k_gather_entry_values<EntryF, T><<<grid_for(t->nslots), 256, 0, st>>>(
+            t->nslots, t->perm.as<int>(), p.val.as<T>(), t->slots.as<EntryF>());
+        after_launch("refresh_slots");
+        if (t->novf) {
+          k_gather_entry_values<EntryF, T><<<grid_for(t->novf), 256, 0, st>>>(
+              t->novf, t->ovf_perm.as<int>(), p.val.as<T>(), t->ovf.as<EntryF>());
+          after_launch("refresh_overflow");
+        }
+      }
+    }
   })
 }
 

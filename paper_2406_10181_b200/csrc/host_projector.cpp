@@ -223,4 +223,57 @@ void build_chunks(int n_rows, int d, int bm, const std::vector<int32_t>& csc_ptr
   split[static_cast<size_t>(nchunks) * d] = static_cast<int32_t>(perm.size());
 }
 
+void build_slots(int n_rows, int d, int bm, int K, int bpw, const std::vector<int32_t>& csc_ptr,
+                 const std::vector<int32_t>& csc_rows, const std::vector<int32_t>& csc_perm,
+                 SlotHost& out) {
+  const int nchunks = ceil_div(n_rows, bm);
+  const int dpad = static_cast<int>(round_up(d, 32));
+  const int nw = dpad / bpw;
+  const size_t nslots = static_cast<size_t>(nchunks) * dpad * K;
+  out.slot_row.assign(nslots, -1);
+  out.slot_perm.assign(nslots, -1);
+  out.ovf_split.assign(static_cast<size_t>(nchunks) * nw + 1, 0);
+  out.ovf_row.clear();
+  out.ovf_bin.clear();
+  out.ovf_perm.clear();
+  std::vector<int32_t> cursor(csc_ptr.begin(), csc_ptr.end() - 1);
+  for (int c = 0; c < nchunks; ++c) {
+    const int lim = (c + 1) * bm;
+    for (int a = 0; a < dpad; ++a) {
+      if (a % bpw == 0)
+        out.ovf_split[static_cast<size_t>(c) * nw + a / bpw] = static_cast<int32_t>(out.ovf_row.size());
+      if (a >= d) continue;
+      int32_t& cu = cursor[a];
+      int t = 0;
+      for (; cu < csc_ptr[a + 1] && csc_rows[cu] < lim; ++cu, ++t) {
+        if (t < K) {
+          const size_t s = (static_cast<size_t>(c) * dpad + a) * K + t;
+          out.slot_row[s] = csc_rows[cu] - c * bm;
+          out.slot_perm[s] = csc_perm[cu];
+        } else {
+          out.ovf_row.push_back(csc_rows[cu] - c * bm);
+          out.ovf_bin.push_back(a % bpw);
+          out.ovf_perm.push_back(csc_perm[cu]);
+        }
+      }
+    }
+  }
+  out.ovf_split.back() = static_cast<int32_t>(out.ovf_row.size());
+}
+
+long long count_overflow(int n_rows, int d, int bm, int K, const std::vector<int32_t>& csc_ptr,
+                         const std::vector<int32_t>& csc_rows) {
+  long long ovf = 0;
+  for (int a = 0; a < d; ++a) {
+    int chunk = -1, t = 0;
+    for (int e = csc_ptr[a]; e < csc_ptr[a + 1]; ++e) {
+      const int c = csc_rows[e] / bm;
+      if (c != chunk) chunk = c, t = 0;
+      if (++t > K) ++ovf;
+    }
+  }
+  (void)n_rows;
+  return ovf;
+}
+
 }  // namespace lspb

@@ -25,4 +25,20 @@ void build_chunks(int n_rows, int d, int bm, const std::vector<int32_t>& csc_ptr
                   std::vector<int32_t>& split, std::vector<int32_t>& row_in_chunk,
                   std::vector<int32_t>& perm);
 
+// Fixed-slot stage-1 table (compress_slots.cu).  Per (row chunk c, bin a) the
+// first K entries of the bin in the chunk (rows ascending) fill
+// slot_row/slot_perm[(c*dpad + a)*K + t] (row -1 / perm -1 = padding); the
+// bin's further entries go to the overflow list of (c, a/bpw), in bin then
+// row order, with ovf_bin = a % bpw.  ovf_split[c*(dpad/bpw) + w] is the
+// first overflow entry of (c, w).  dpad = d rounded up to 32; bpw divides 32.
+struct SlotHost {
+  std::vector<int32_t> slot_row, slot_perm, ovf_split, ovf_row, ovf_bin, ovf_perm;
+};
+void build_slots(int n_rows, int d, int bm, int K, int bpw, const std::vector<int32_t>& csc_ptr,
+                 const std::vector<int32_t>& csc_rows, const std::vector<int32_t>& csc_perm,
+                 SlotHost& out);
+// Entries that would not fit K slots per (chunk, bin), i.e. the overflow size.
+long long count_overflow(int n_rows, int d, int bm, int K, const std::vector<int32_t>& csc_ptr,
+                         const std::vector<int32_t>& csc_rows);
+
 }  // namespace lspb

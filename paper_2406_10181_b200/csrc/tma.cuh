@@ -12,6 +12,9 @@ namespace lspb {
 // (alignment etc.), so callers can fall back to cp.async.
 bool encode_tmap_2d(CUtensorMap* map, const void* base, lsp_dtype dt, long long rows,
                     long long cols, long long ld_elems, int box_cols, int box_rows);
+// encode_tmap_2d behind a process-wide cache keyed on every argument.
+bool cached_tmap(CUtensorMap* out, const void* base, lsp_dtype dt, long long rows, long long cols,
+                 long long ld, int bc, int br);
 
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned smem_addr(const void* p) {

@@ -337,3 +337,58 @@ def test_decompress_paths_agree(cuda, port, generic, monkeypatch):
         assert rel(host(w) - w0, ref - w0) < 1e-5
         out = host(pair.decompress(dev(delta)))
         assert rel(out, port.decompress(P, Q, delta)) < 1e-5
+
+
+def _skewed(m, d, r, seed, hot):
+    """A structured projector: every row hits the `hot` lowest bins first, so a
+    few bins collect most entries (stress for the fixed-slot overflow lists)."""
+    rng = np.random.default_rng(seed)
+    pos = np.empty((m, r), np.int32)
+    for i in range(m):
+        lo = rng.choice(hot, size=min(r, hot), replace=False)
+        rest = rng.choice(np.arange(hot, d), size=r - len(lo), replace=False) if r > hot else []
+        pos[i] = np.sort(np.concatenate([lo, rest]).astype(np.int32))
+    val = rng.standard_normal((m, r)) / np.sqrt(r)
+    return oracle.Projector(m, d, r, pos.ravel(), val.ravel())
+
+
+@pytest.mark.parametrize("pin", ["", "1,2", "1,4", "1,8", "2,2", "2,4"])
+@pytest.mark.parametrize("gdt", ["f32", "bf16"])
+def test_compress_paths_agree(cuda, port, gdt, pin, monkeypatch):
+    """Fixed-slot TMA stage 1 vs the CSC-walk stage 1: bitwise identical (same
+    per-bin summation order), both on the oracle; random and skewed projectors,
+    ragged m and n, d not a multiple of 32; every (columns per lane, K) variant."""
+    monkeypatch.setenv("LSP_COMPRESS_SLOTS", pin)
+    cases = []
+    for (m, n, d, r) in [(777, 1000, 64, 4), (1300, 4100, 128, 4), (4096, 96, 1024, 4),
+                         (513, 257, 100, 3), (2000, 300, 2048, 4)]:
+        P, Q, _ = make(port, m, n, d, r, m + n)
+        cases.append((P, Q))
+    for hot in (1, 3):
+        cases.append((_skewed(1500, 96, 4, hot, hot), port.init_sparse(700, 96, 4, 5)))
+    for P, Q in cases:
+        g = f32normal(P.n_rows, (P.n_rows, Q.n_rows))
+        if gdt == "bf16":
+            g = bf16_round(g)
+        outs = []
+        for generic in ("0", "1"):
+            monkeypatch.setenv("LSP_COMPRESS_GENERIC", generic)
+            pair = lsp.DevicePair(lsp.DeviceProjector(P.n_rows, P.d, P.r, P.pos, P.val),
+                                  lsp.DeviceProjector(Q.n_rows, Q.d, Q.r, Q.pos, Q.val))
+            outs.append(pair.compress(dev(g, gdt)).clone())
+        assert torch.equal(outs[0], outs[1])
+        assert rel(host(outs[0]), port.compress(P, Q, g)) < 1e-5
+
+
+def test_compress_slots_value_refresh(cuda, port):
+    """set_values re-derives the slot and overflow tables' values on the device."""
+    P = _skewed(900, 64, 4, 11, 2)
+    Q = port.init_sparse(300, 64, 4, 12)
+    dp = lsp.DeviceProjector(P.n_rows, P.d, P.r, P.pos, P.val)
+    pair = lsp.DevicePair(dp, lsp.DeviceProjector(Q.n_rows, Q.d, Q.r, Q.pos, Q.val))
+    g = f32normal(4, (900, 300))
+    pair.compress(dev(g))  # builds the tables
+    P2 = P.copy()
+    P2.val = np.random.default_rng(3).standard_normal(P.val.shape)
+    dp.set_values(P2.val)
+    assert rel(host(pair.compress(dev(g))), port.compress(P2, Q, g)) < 1e-5
