@@ -1,0 +1,646 @@
+// Fused decompress-and-apply, two-kernel form for fp32 accumulation
+// (reference: rightT_mul proj/src/projector.cpp:148-161, left_mul :105-117,
+//  decompress :170-175, apply W -= lr * decompress proj/src/trainer.cpp:190):
+//
+//   out = beta * in + alpha * P (Delta Q^T)
+//
+// 1. k_build_y: Y = Delta Q^T (d x n) is computed ONCE per matrix into a
+//    band-blocked workspace Yb[band][a][jj] (BN columns per band, so every
+//    band is one contiguous d x BN block).  Y[a][j] = sum_l q(j,l) *
+//    Delta^T[pos_q(j,l)][a]: row gathers of the L2-resident Delta^T, 128-byte
+//    coalesced per warp, the l-sum in the reference's order.
+// 2. k_apply_y: persistent streaming kernel, one CTA per SM, stream-K split
+//    of the (matrix, band, row-block) tile list.  Warp 0 streams W tiles (2-D
+//    TMA, evict-first) and the tile rows' CSR entries of P (bulk copies)
+//    through an S-stage mbarrier ring; warp 1 bulk-copies the band's Y block
+//    into shared memory whenever the CTA enters a new band (no arithmetic,
+//    no block-wide barrier); 16 consumer warps do, per W element, k
+//    conflict-free shared-memory gathers Y[pos_p(i,l)][jj] and one
+//    read-modify-write of W.  W is read and written exactly once.
+//
+// Compared with building Y_band inside the apply kernel (decompress_tma.cu),
+// the per-band cost drops from r*BN row gathers of Delta^T (512 KB of L2
+// traffic plus the FMAs, during which the W stream stalls) to one 128 KB bulk
+// copy that overlaps the ring.  Arithmetic and summation order are unchanged,
+// so results are bitwise those of the other decompress kernels.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "core.cuh"
+#include "tma.cuh"
+
+namespace lspb {
+
+namespace {
+
+constexpr int kYMaxBytes = 160 * 1024;  // Y block of one band in shared memory
+constexpr int kSmemMax = 227 * 1024;
+constexpr int kNC = 16;                 // consumer warps
+constexpr int kNG = 2;                  // consumer groups
+constexpr int kAThreads = (kNC + 2) * 32;
+constexpr int kMaxStages = 16;
+constexpr int kYChunk = 16 * 1024;      // bulk-copy granule for the Y block
+constexpr int kTileElems = 4096;        // W elements per ring tile (BN x TR)
+
+// ---------------------------------------------------------------------------
+// Y build
+// ---------------------------------------------------------------------------
+struct YMat {
+  const int* qpos;
+  const float* qval;
+  const float* dT;  // Delta^T: element (a, b) of Delta at b*d + a
+  float* yb;
+  int n, nbands;
+  long long task_end;
+};
+struct YArgs {
+  YMat mat[kMaxGroup];
+  int count, d, ablocks;
+  long long total;
+  const int* skip;
+};
+
+// One warp = one (matrix, band, 64-row block of a).  Lane owns a0+lane and
+// a0+32+lane; the band's BN columns are unrolled into registers so every
+// output row segment (BN floats) is written with contiguous 16-byte stores.
+template <int BN, int KR>
+__global__ void __launch_bounds__(256) k_build_y(const __grid_constant__ YArgs A) {
+  if (A.skip && *A.skip) return;
+  const int lane = threadIdx.x & 31;
+  const long long task = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (task >= A.total) return;
+  int mi = 0;
+  while (mi + 1 < A.count && task >= A.mat[mi].task_end) ++mi;
+  const YMat& M = A.mat[mi];
+  const long long lt = task - (mi ? A.mat[mi - 1].task_end : 0);
+  const int band = static_cast<int>(lt / A.ablocks);
+  const int a0 = static_cast<int>(lt % A.ablocks) * 64;
+  const int d = A.d;
+  const int a_lo = a0 + lane, a_hi = a0 + 32 + lane;
+  const bool ok_lo = a_lo < d, ok_hi = a_hi < d;
+  float y0[BN], y1[BN];
+#pragma unroll
+  for (int jj = 0; jj < BN; ++jj) {
+    y0[jj] = 0.0f;
+    y1[jj] = 0.0f;
+    const int j = band * BN + jj;
+    if (j < M.n) {
+      int p[KR];
+      float q[KR];
+      if constexpr (KR % 4 == 0) {
+#pragma unroll
+        for (int l = 0; l < KR; l += 4) {
+          const int4 pv = __ldg(reinterpret_cast<const int4*>(M.qpos + static_cast<long long>(j) * KR + l));
+          const float4 qv = __ldg(reinterpret_cast<const float4*>(M.qval + static_cast<long long>(j) * KR + l));
+          p[l] = pv.x, p[l + 1] = pv.y, p[l + 2] = pv.z, p[l + 3] = pv.w;
+          q[l] = qv.x, q[l + 1] = qv.y, q[l + 2] = qv.z, q[l + 3] = qv.w;
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < KR; ++l) {
+          p[l] = __ldg(M.qpos + static_cast<long long>(j) * KR + l);
+          q[l] = __ldg(M.qval + static_cast<long long>(j) * KR + l);
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < KR; ++l) {
+        const float* row = M.dT + static_cast<long long>(p[l]) * d;
+        if (ok_lo) y0[jj] = fmaf(q[l], __ldg(row + a_lo), y0[jj]);
+        if (ok_hi) y1[jj] = fmaf(q[l], __ldg(row + a_hi), y1[jj]);
+      }
+    }
+  }
+  float* base = M.yb + static_cast<long long>(band) * d * BN;
+  if (ok_lo) {
+    float4* o = reinterpret_cast<float4*>(base + static_cast<long long>(a_lo) * BN);
+#pragma unroll
+    for (int t = 0; t < BN / 4; ++t)
+      o[t] = make_float4(y0[4 * t], y0[4 * t + 1], y0[4 * t + 2], y0[4 * t + 3]);
+  }
+  if (ok_hi) {
+    float4* o = reinterpret_cast<float4*>(base + static_cast<long long>(a_hi) * BN);
+#pragma unroll
+    for (int t = 0; t < BN / 4; ++t)
+      o[t] = make_float4(y1[4 * t], y1[4 * t + 1], y1[4 * t + 2], y1[4 * t + 3]);
+  }
+}
+
+// Shared-memory form (d <= kDsMaxD): a CTA stages the 32 columns a0..a0+31 of
+// Delta (= rows of Delta^T restricted to a0..a0+31, d x 128 B) once and
+// computes Yb[band][a0 + lane][0..BN) for a contiguous range of bands with
+// conflict-free shared-memory gathers (lane = a).  Work units are (matrix,
+// a-block, chunk of kYBands bands), dealt as contiguous ranges so a CTA
+// re-stages Delta only when its (matrix, a-block) changes.
+constexpr int kYBands = 16;
+constexpr int kYWarps = 16;
+constexpr int kDsMaxD = 1536;
+
+struct Y2Args {
+  YMat mat[kMaxGroup];
+  int count, d, ablocks;
+  long long units;  // mat[i].task_end: cumulative units
+  const int* skip;
+};
+
+template <int BN, int KR>
+__global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_constant__ Y2Args A) {
+  constexpr int NQ = BN * KR / 4;          // int4 (and float4) entry chunks per band
+  constexpr int NE = (NQ + 31) / 32;       // per lane
+  extern __shared__ __align__(16) float ds[];  // [d][32], then per-warp entry areas
+  if (A.skip && *A.skip) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = A.d;
+  int4* epos = reinterpret_cast<int4*>(ds + d * 32) + warp * 2 * NQ;  // [NQ] pos, then [NQ] val
+  const long long u_begin = A.units * blockIdx.x / gridDim.x;
+  const long long u_end = A.units * (blockIdx.x + 1) / gridDim.x;
+  int cur_mi = -1, cur_ab = -1;
+  for (long long u = u_begin; u < u_end; ++u) {
+    int mi = 0;
+    while (mi + 1 < A.count && u >= A.mat[mi].task_end) ++mi;
+    const YMat& M = A.mat[mi];
+    const long long lt = u - (mi ? A.mat[mi - 1].task_end : 0);
+    const int nchunks = (M.nbands + kYBands - 1) / kYBands;
+    const int ab = static_cast<int>(lt / nchunks);
+    const int chunk = static_cast<int>(lt % nchunks);
+    const int a0 = ab * 32;
+    if (mi != cur_mi || ab != cur_ab) {
+      __syncthreads();  // previous block fully consumed
+      // ds[b][t] = Delta^T[b][a0 + t]  (zero beyond d); 8 loads in flight per thread
+      for (int i0 = threadIdx.x; i0 < d * 8; i0 += 8 * blockDim.x) {
+        float4 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int idx = i0 + e * blockDim.x;
+          const int b = idx >> 3, q = (idx & 7) * 4;
+          v[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (idx < d * 8) {
+            const float* src = M.dT + static_cast<long long>(b) * d + a0 + q;
+            if (a0 + q + 3 < d) {
+              v[e] = __ldg(reinterpret_cast<const float4*>(src));
+            } else {
+              if (a0 + q < d) v[e].x = src[0];
+              if (a0 + q + 1 < d) v[e].y = src[1];
+              if (a0 + q + 2 < d) v[e].z = src[2];
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int idx = i0 + e * blockDim.x;
+          if (idx < d * 8) *reinterpret_cast<float4*>(ds + (idx >> 3) * 32 + (idx & 7) * 4) = v[e];
+        }
+      }
+      __syncthreads();
+      cur_mi = mi;
+      cur_ab = ab;
+    }
+    const int a = a0 + lane;
+    const int band_end = min(M.nbands, (chunk + 1) * kYBands);
+    // the band's BN*KR (pos, val) pairs are contiguous in the CSR arrays of Q
+    const long long qlim = static_cast<long long>(M.n) * KR;
+    auto fetch = [&](int band, int4 (&pr)[NE], float4 (&vr)[NE]) {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int t = lane + 32 * e;
+        const long long off = static_cast<long long>(band) * BN * KR + 4LL * t;
+        pr[e] = make_int4(0, 0, 0, 0);
+        vr[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < NQ && band < band_end && off < qlim) {
+          pr[e] = __ldg(reinterpret_cast<const int4*>(M.qpos + off));
+          vr[e] = __ldg(reinterpret_cast<const float4*>(M.qval + off));
+        }
+      }
+    };
+    int4 pr[NE];
+    float4 vr[NE];
+    int band = chunk * kYBands + warp;
+    fetch(band, pr, vr);
+    for (; band < band_end; band += kYWarps) {
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int t = lane + 32 * e;
+        if (t < NQ) {
+          epos[t] = pr[e];
+          reinterpret_cast<float4*>(epos + NQ)[t] = vr[e];
+        }
+      }
+      __syncwarp();
+      fetch(band + kYWarps, pr, vr);  // next band's entries in flight
+      const int* sp = reinterpret_cast<const int*>(epos);
+      const float* sv = reinterpret_cast<const float*>(epos + NQ);
+      float y[BN];
+#pragma unroll
+      for (int jj = 0; jj < BN; ++jj) {
+        // columns beyond n have zero entries (fetch), so y stays 0: no branch,
+        // the BN column chains interleave freely
+        y[jj] = 0.0f;
+#pragma unroll
+        for (int l = 0; l < KR; l += 4) {
+          const int4 pv = *reinterpret_cast<const int4*>(sp + jj * KR + l);
+          const float4 qv = *reinterpret_cast<const float4*>(sv + jj * KR + l);
+          y[jj] = fmaf(qv.x, ds[pv.x * 32 + lane], y[jj]);
+          y[jj] = fmaf(qv.y, ds[pv.y * 32 + lane], y[jj]);
+          y[jj] = fmaf(qv.z, ds[pv.z * 32 + lane], y[jj]);
+          y[jj] = fmaf(qv.w, ds[pv.w * 32 + lane], y[jj]);
+        }
+      }
+      if (a < d) {
+        float4* o = reinterpret_cast<float4*>(M.yb + (static_cast<long long>(band) * d + a) * BN);
+#pragma unroll
+        for (int t = 0; t < BN / 4; ++t)
+          o[t] = make_float4(y[4 * t], y[4 * t + 1], y[4 * t + 2], y[4 * t + 3]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// streaming apply
+// ---------------------------------------------------------------------------
+struct alignas(64) AMat {
+  CUtensorMap tmap;        // W (input) tile map: box BN x TR
+  const int* ppos_scaled;  // P positions * BN * 4: byte offsets of Y rows
+  const float* pval;
+  const float* yb;
+  void* out;
+  long long ldo;
+  int m, n, row_blocks, nbands, rps;  // rps: row blocks per unit (row segment)
+  long long unit_end;
+};
+struct AArgs {
+  AMat mat[kMaxGroup];
+  int count, d, stages, stage_bytes, y_bytes, w_bytes, e_bytes, pf;
+  long long units;
+  double alpha, beta;
+  const int* skip;
+};
+
+// A unit = (matrix, row segment, band): the band's Y block is loaded once per
+// unit.  Units are ordered (matrix, segment, band) and dealt round-robin to
+// the CTAs, so the units in flight at any moment are ADJACENT bands of the
+// same rows: together they read and write contiguous row spans of W (DRAM
+// page locality), while each CTA still walks down its own band.
+struct Unit {
+  int mi, band, rb0, rb1;
+};
+__device__ __forceinline__ Unit unit_at(const AArgs& A, long long u) {
+  int i = 0;
+  while (i + 1 < A.count && u >= A.mat[i].unit_end) ++i;
+  const AMat& M = A.mat[i];
+  const long long lt = u - (i ? A.mat[i - 1].unit_end : 0);
+  const int seg = static_cast<int>(lt / M.nbands);
+  const int rb0 = seg * M.rps;
+  return Unit{i, static_cast<int>(lt % M.nbands), rb0, min(M.row_blocks, rb0 + M.rps)};
+}
+
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int4 lds_v4i(unsigned addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float4 lds_v4f(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+template <typename Tw>
+__device__ __forceinline__ float lds_w(unsigned addr) {
+  if constexpr (std::is_same<Tw, float>::value) {
+    return lds_f32(addr);
+  } else {
+    unsigned short h;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(addr));
+    return __uint_as_float(static_cast<unsigned>(h) << 16);
+  }
+}
+
+template <typename Tw, int BN, int KR, bool USE_IN>
+__global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant__ AArgs A) {
+  constexpr int TR = kTileElems / BN < 256 ? kTileElems / BN : 256;  // W rows per tile
+  constexpr int RPW = 32 / BN;         // rows per warp instruction
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  if (A.skip && *A.skip) return;
+  // consumer warps form kNG groups; group g takes tiles g, g+kNG, ... so kNG
+  // tiles are consumed concurrently (a tile's latency is not serialised)
+  unsigned char* ring = smem_raw + A.y_bytes;
+  unsigned long long* full =
+      reinterpret_cast<unsigned long long*>(ring + A.stages * A.stage_bytes);
+  unsigned long long* empty = full + A.stages;
+  unsigned long long* yfull = empty + A.stages;
+  unsigned long long* yempty = yfull + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int S = A.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kNC / kNG);
+    }
+    mbar_init(yfull, 1);
+    mbar_init(yempty, kNC);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (blockIdx.x >= A.units) return;
+
+  if (warp == 0) {
+    // ---------------- W / P-entry producer ----------------
+    if (lane == 0) {
+      const unsigned long long pol = policy_evict_first();
+      int s = 0;
+      for (long long u = blockIdx.x; u < A.units; u += gridDim.x) {
+        const Unit U = unit_at(A, u);
+        const AMat& M = A.mat[U.mi];
+        if (USE_IN && A.pf > S)  // fill the L2 prefetch window beyond the ring
+          for (int rb = U.rb0 + S; rb < min(U.rb1, U.rb0 + A.pf); ++rb)
+            tma_prefetch_2d(&M.tmap, U.band * BN, rb * TR);
+        for (int rb = U.rb0; rb < U.rb1; ++rb, ++s) {
+          const int st = s % S;
+          if (USE_IN && A.pf > S && rb + A.pf < U.rb1)
+            tma_prefetch_2d(&M.tmap, U.band * BN, (rb + A.pf) * TR);
+          if (s >= S) mbar_wait(empty + st, ((s / S) - 1) & 1);
+          const int r0 = rb * TR;
+          const int nrows = min(TR, M.m - r0);
+          unsigned char* base = ring + st * A.stage_bytes;
+          const unsigned eb = static_cast<unsigned>(nrows) * KR * 4u;
+          mbar_arrive_expect_tx(full + st, (USE_IN ? A.w_bytes : 0) + 2u * eb);
+          if (USE_IN) tma_load_2d(base, &M.tmap, U.band * BN, r0, full + st, pol);
+          bulk_load(base + A.w_bytes, M.ppos_scaled + static_cast<long long>(r0) * KR, eb,
+                    full + st);
+          bulk_load(base + A.w_bytes + A.e_bytes, M.pval + static_cast<long long>(r0) * KR, eb,
+                    full + st);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1) {
+    // ---------------- Y block producer (one bulk copy per unit) ----------------
+    if (lane == 0) {
+      int k = 0;
+      for (long long u = blockIdx.x; u < A.units; u += gridDim.x, ++k) {
+        const Unit U = unit_at(A, u);
+        if (k > 0) mbar_wait(yempty, (k - 1) & 1);
+        mbar_arrive_expect_tx(yfull, static_cast<unsigned>(A.y_bytes));
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(
+            A.mat[U.mi].yb + static_cast<long long>(U.band) * A.d * BN);
+        for (int off = 0; off < A.y_bytes; off += kYChunk)
+          bulk_load(smem_raw + off, src + off, min(kYChunk, A.y_bytes - off), yfull);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  constexpr int WPG = kNC / kNG;          // warps per consumer group
+  constexpr int RPT = TR / (WPG * RPW);   // rows per lane per tile
+  const int cw = warp - 2;
+  const int grp = cw / WPG, gw = cw % WPG;
+  const float alpha = static_cast<float>(A.alpha), beta = static_cast<float>(A.beta);
+  const int jj = lane % BN, rsub = lane / BN;
+  const int q0 = gw * RPW + rsub;  // this lane's first row in a tile; rows q0 + v*WPG*RPW
+  const unsigned y_lane = smem_addr(smem_raw) + jj * 4u;
+  const unsigned ring_s = smem_addr(ring);
+  int s = 0, k = 0;
+  for (long long u = blockIdx.x; u < A.units; u += gridDim.x, ++k) {
+    const Unit U = unit_at(A, u);
+    const AMat& M = A.mat[U.mi];
+    const int j = U.band * BN + jj;
+    const bool col_ok = j < M.n;
+    Tw* const ocol = static_cast<Tw*>(M.out) + j;  // element offsets below fit in 32 bits
+    const int ldo = static_cast<int>(M.ldo);
+    mbar_wait(yfull, k & 1);
+    for (int rb = U.rb0; rb < U.rb1; ++rb, ++s) {
+      if (s % kNG != grp) continue;
+      const int st = s % S;
+      const int r0 = rb * TR;
+      const int nrows = min(TR, M.m - r0);
+      mbar_wait(full + st, (s / S) & 1);
+      const unsigned base = ring_s + st * A.stage_bytes;
+      const unsigned wq = base + (q0 * BN + jj) * static_cast<unsigned>(sizeof(Tw));
+      const unsigned pq = base + A.w_bytes + q0 * KR * 4u;
+      const unsigned vq = base + A.w_bytes + A.e_bytes + q0 * KR * 4u;
+      constexpr int kq = WPG * RPW;  // row step between a lane's rows
+      auto row = [&](int v) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int l = 0; l < KR; l += 4) {
+          const int4 pp = lds_v4i(pq + (v * kq * KR + l) * 4u);
+          const float4 vv = lds_v4f(vq + (v * kq * KR + l) * 4u);
+          acc = l == 0 ? vv.x * lds_f32(y_lane + pp.x) : fmaf(vv.x, lds_f32(y_lane + pp.x), acc);
+          acc = fmaf(vv.y, lds_f32(y_lane + pp.y), acc);
+          acc = fmaf(vv.z, lds_f32(y_lane + pp.z), acc);
+          acc = fmaf(vv.w, lds_f32(y_lane + pp.w), acc);
+        }
+        float res = alpha * acc;
+        if (USE_IN) res = fmaf(beta, lds_w<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw))), res);
+        return cvt<Tw>(res);
+      };
+      if (col_ok) {
+        Tw* const orow = ocol + static_cast<long long>(r0 + q0) * ldo;
+        if (nrows == TR) {  // straight-line: rows interleave freely
+          const int stride = kq * ldo;
+#pragma unroll
+          for (int v = 0; v < RPT; ++v) orow[v * stride] = row(v);
+        } else {
+#pragma unroll 1
+          for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
+            orow[static_cast<long long>(v) * kq * ldo] = row(v);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+    }
+    if (lane == 0) mbar_arrive(yempty);  // this unit's Y block may be replaced
+  }
+}
+
+template <int BN, int KR>
+void build_y_impl(const std::vector<DecJob>& jobs, const int* skip, cudaStream_t st) {
+  const Pair& p0 = *jobs[0].pr;
+  const char* env = std::getenv("LSP_BUILD_Y_GLOBAL");
+  const bool use_smem = p0.d <= kDsMaxD && !(env && env[0] == '1');
+  YArgs A{};
+  Y2Args B{};
+  A.count = B.count = static_cast<int>(jobs.size());
+  A.d = B.d = p0.d;
+  A.ablocks = ceil_div(p0.d, 64);
+  B.ablocks = ceil_div(p0.d, 32);
+  A.skip = B.skip = skip;
+  long long total = 0, units = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const Pair& pr = *jobs[i].pr;
+    YMat M{};
+    M.qpos = pr.q->pos.as<int>();
+    M.qval = pr.q->val.as<float>();
+    M.dT = static_cast<const float*>(jobs[i].delta_t);
+    M.yb = pr.yb.as<float>();
+    M.n = pr.n;
+    M.nbands = ceil_div(pr.n, BN);
+    total += static_cast<long long>(M.nbands) * A.ablocks;
+    units += static_cast<long long>(ceil_div(M.nbands, kYBands)) * B.ablocks;
+    M.task_end = total;
+    A.mat[i] = M;
+    M.task_end = units;
+    B.mat[i] = M;
+  }
+  A.total = total;
+  B.units = units;
+  if (total == 0) return;
+  if (use_smem) {
+    const int smem = p0.d * 32 * static_cast<int>(sizeof(float)) + kYWarps * 2 * BN * KR * 4;
+    auto kern = k_build_y_smem<BN, KR>;
+    LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int grid = static_cast<int>(std::min<long long>(units, num_sms()));
+    kern<<<grid, kYWarps * 32, smem, st>>>(B);
+    after_launch("build_y_smem");
+    return;
+  }
+  k_build_y<BN, KR><<<static_cast<unsigned>((total + 7) / 8), 256, 0, st>>>(A);
+  after_launch("build_y");
+}
+
+template <typename Tw, int BN, int KR>
+bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, const int* skip,
+                cudaStream_t st) {
+  constexpr int TR = kTileElems / BN < 256 ? kTileElems / BN : 256;
+  const Pair& p0 = *jobs[0].pr;
+  const bool use_in = beta != 0.0;
+  AArgs A{};
+  A.count = static_cast<int>(jobs.size());
+  A.d = p0.d;
+  A.alpha = alpha;
+  A.beta = beta;
+  A.skip = skip;
+  A.y_bytes = p0.d * BN * 4;
+  A.w_bytes = TR * BN * static_cast<int>(sizeof(Tw));
+  A.e_bytes = TR * KR * 4;
+  A.stage_bytes = static_cast<int>(round_up(A.w_bytes + 2 * A.e_bytes, 128));
+  const int bar_bytes = (2 * kMaxStages + 2) * 8;
+  A.stages = std::min(kMaxStages, (kSmemMax - A.y_bytes - bar_bytes) / A.stage_bytes);
+  if (const char* e = std::getenv("LSP_APPLY_STAGES")) A.stages = std::min(A.stages, std::atoi(e));
+  if (A.stages < 3) return false;
+  A.pf = 0;  // L2 prefetch distance in tiles (0: off)
+  if (const char* e = std::getenv("LSP_APPLY_PF")) A.pf = std::atoi(e);
+  const int grid_max = num_sms();
+  long long tiles = 0;
+  for (const DecJob& J : jobs)
+    tiles += static_cast<long long>(ceil_div(J.pr->n, BN)) * ceil_div(J.pr->m, TR);
+  // unit (row segment of a band) at most ~1/4 of a CTA's share, so the
+  // round-robin deal stays balanced; env LSP_APPLY_SEG overrides (rows blocks)
+  long long cap = std::max<long long>(8, tiles / grid_max / 4);
+  if (const char* e = std::getenv("LSP_APPLY_SEG")) cap = std::max(1, std::atoi(e));
+  long long units = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const DecJob& J = jobs[i];
+    const Pair& pr = *J.pr;
+    AMat& M = A.mat[i];
+    if (use_in && !cached_tmap(&M.tmap, J.in, std::is_same<Tw, float>::value ? LSP_F32 : LSP_BF16,
+                               pr.m, pr.n, J.ldi, BN, TR))
+      return false;
+    M.ppos_scaled = pr.p->scaled_pos(BN * 4);
+    M.pval = pr.p->val.as<float>();
+    M.yb = pr.yb.as<float>();
+    M.out = J.out;
+    M.ldo = J.ldo;
+    M.m = pr.m, M.n = pr.n;
+    M.row_blocks = ceil_div(pr.m, TR);
+    M.nbands = ceil_div(pr.n, BN);
+    const int segs = ceil_div(M.row_blocks, cap);
+    M.rps = ceil_div(M.row_blocks, segs);
+    units += static_cast<long long>(M.nbands) * ceil_div(M.row_blocks, M.rps);
+    M.unit_end = units;
+  }
+  A.units = units;
+  if (units == 0) return true;
+  const int smem = A.y_bytes + A.stages * A.stage_bytes + bar_bytes;
+  auto kern = use_in ? k_apply_y<Tw, BN, KR, true> : k_apply_y<Tw, BN, KR, false>;
+  LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = static_cast<int>(std::min<long long>(units, grid_max));
+  kern<<<grid, kAThreads, smem, st>>>(A);
+  after_launch("apply_y");
+  return true;
+}
+
+template <int BN, int KR>
+bool run_bn(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha, double beta,
+            const int* skip, cudaStream_t st) {
+  for (const DecJob& J : jobs) {
+    const Pair& pr = *J.pr;
+    J.pr->yb_ensure(static_cast<size_t>(ceil_div(pr.n, BN)) * pr.d * BN * sizeof(float));
+  }
+  // check eligibility of the apply before enqueueing the Y build
+  for (const DecJob& J : jobs)  // 32-bit element offsets into W
+    if (static_cast<long long>(J.pr->m) * J.ldo >= (1LL << 31)) return false;
+  if (beta != 0.0)
+    for (const DecJob& J : jobs) {
+      if (J.in == nullptr) return false;
+      const size_t es = dtype_size(dt);
+      if (reinterpret_cast<uintptr_t>(J.in) % 16 || (J.ldi * es) % 16) return false;
+    }
+  // Y build + apply per subgroup whose Y blocks fit comfortably in L2, so the
+  // apply reads Y from L2 rather than HBM (env LSP_APPLY_YB_MB, default 64)
+  size_t budget = 64ull << 20;
+  if (const char* e = std::getenv("LSP_APPLY_YB_MB")) budget = static_cast<size_t>(std::atoi(e)) << 20;
+  size_t i = 0;
+  while (i < jobs.size()) {
+    size_t j = i, bytes = 0;
+    while (j < jobs.size()) {
+      const Pair& pr = *jobs[j].pr;
+      const size_t b = static_cast<size_t>(ceil_div(pr.n, BN)) * pr.d * BN * sizeof(float);
+      if (j > i && bytes + b > budget) break;
+      bytes += b;
+      ++j;
+    }
+    const std::vector<DecJob> sub(jobs.begin() + i, jobs.begin() + j);
+    build_y_impl<BN, KR>(sub, skip, st);
+    const bool ok = dt == LSP_F32 ? apply_impl<float, BN, KR>(sub, alpha, beta, skip, st)
+                                  : apply_impl<bf16, BN, KR>(sub, alpha, beta, skip, st);
+    require(ok, "apply_y: launch configuration rejected after the Y build");
+    i = j;
+  }
+  return true;
+}
+
+}  // namespace
+
+// Fast path of launch_decompress_group for fp32 accumulation, W in fp32 or
+// bf16, r in {4, 8}; false (nothing enqueued) when not eligible.
+bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
+                               double beta, const int* skip_flag, cudaStream_t st) {
+  if (jobs.empty() || jobs.size() > static_cast<size_t>(kMaxGroup)) return false;
+  const Pair& p0 = *jobs[0].pr;
+  if (p0.compute != LSP_F32 || (dt != LSP_F32 && dt != LSP_BF16)) return false;
+  const int r = p0.p->r;
+  if (r != 4 && r != 8) return false;
+  for (const DecJob& J : jobs)
+    if (J.pr->q->r != r || J.pr->p->r != r) return false;
+  const int d = p0.d;
+  auto pick = [&](auto bn) -> bool {
+    constexpr int BN = decltype(bn)::value;
+    return r == 4 ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st)
+                  : run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st);
+  };
+  const char* bn_env = std::getenv("LSP_APPLY_BN");
+  const int bn_max = bn_env ? std::atoi(bn_env) : 32;
+  if (bn_max >= 32 && d * 32 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 32>{});
+  if (bn_max >= 16 && d * 16 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 16>{});
+  if (d * 16 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 16>{});
+  if (d * 8 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 8>{});
+  return false;
+}
+
+}  // namespace lspb

@@ -27,6 +27,14 @@ size_t dtype_size(lsp_dtype t) {
   fail(LSP_EINVAL, "unknown dtype");
 }
 
+bool trace_launches() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSP_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int num_sms() {
   static int sms = [] {
     int dev = 0, v = 0;
@@ -152,6 +160,21 @@ const int* Projector::scaled_pos(int scale) {
   upload(*buf, sp.data(), sp.size() * sizeof(int32_t));
   scaled.emplace_back(scale, std::move(buf));
   return scaled.back().second->as<int>();
+}
+
+const EntryF* Projector::csc_entries() {
+  require(compute == LSP_F32, "csc_entries: fp32 projectors only");
+  if (!csc_ent.p) {
+    std::vector<EntryF> e(nnz() + 2);  // +16 B: 16-byte bulk copies may read past the end
+    for (size_t k = 0; k < nnz(); ++k) {
+      e[k].off = h_csc_rows[k];
+      e[k].val = 0.0f;
+    }
+    upload(csc_ent, e.data(), e.size() * sizeof(EntryF));
+    launch_refresh_values(*this, nullptr);  // values from the device CSR array
+    LSP_CUDA(cudaDeviceSynchronize());
+  }
+  return csc_ent.as<EntryF>();
 }
 
 int* Pair::flag_ptr() {

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -36,10 +38,13 @@ inline void require(bool ok, const std::string& msg) {
 
 extern std::atomic<uint64_t> g_launches;
 // Call after every kernel launch: surfaces launch errors and counts launches.
+// LSP_TRACE=1 prints every launch's name to stderr (debugging aid).
+bool trace_launches();
 inline void after_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(LSP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (trace_launches()) fprintf(stderr, "[lsp] launch %s\n", what);
 }
 
 inline cudaStream_t as_stream(lsp_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -261,6 +261,7 @@ void launch_compress_stage1_group(const std::vector<S1Job>& jobs, lsp_dtype gdt,
                                   cudaStream_t st) {
   if (jobs.empty()) return;
   require(jobs.size() <= static_cast<size_t>(kMaxGroup), "group too large");
+  if (launch_compress_spmm_group(jobs, gdt, st)) return;
   if (launch_compress_slots_group(jobs, gdt, st)) return;
   const Pair& p0 = *jobs[0].pr;
   LSP_DISPATCH_ACC(p0.compute, Tacc, {

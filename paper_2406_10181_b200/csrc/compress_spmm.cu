@@ -1,0 +1,290 @@
+// Compress stage 1, gather form: Z^T = G^T P (n x d) for fp32 accumulation of
+// fp32 / bf16 G (reference: the G^T P half of S = P^T G Q,
+// proj/src/projector.cpp:119-168; compress :163-168).
+//
+// Z[b][:] = sum_{i in CSC_P(b)} p(i,b) * G[i][:] is a sparse x dense product
+// whose sparse factor has ~m*r/d entries per output row.  One warp computes
+// one bin b for one column tile (128 fp32 / 256 bf16 columns, 16 bytes per
+// lane): it walks the bin's CSC entries (rows ascending, the reference's
+// summation order) and gathers the 512-byte row segments G[i][tile] straight
+// from global memory with 16-byte loads, U of them in flight per warp.  The
+// 32 CTAs that cover the bin groups of one column tile run together, so each
+// G tile is fetched from HBM once and re-read r times from L2; there is no
+// shared-memory staging of G, no padding and no overflow path, and warps of a
+// CTA never wait on each other inside a bin.  A CTA owns one (column tile,
+// 32-bin group) item at a time and writes its Z^T block (tile rows x 32 bins,
+// 128-byte row segments) through a shared-memory transpose.
+//
+// Persistent grid; items are ordered (matrix, column tile, bin group) and
+// handed out with a stride of gridDim.x, so the tiles in flight at any moment
+// are a small L2-resident window of G.
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "core.cuh"
+#include "tma.cuh"
+
+namespace lspb {
+
+namespace {
+
+constexpr int kBG = 32;      // bins per item
+constexpr int kSWarps = 16;  // warps per CTA
+constexpr int kSThreads = kSWarps * 32;
+
+struct alignas(64) PMat {
+  CUtensorMap tmap;     // G, box CT columns x prow rows (L2 prefetch only)
+  const void* g;
+  long long ldg;
+  const int* ptr;       // CSC_P offsets [d + 1]
+  const EntryF* ent;    // CSC_P entries {row, value}
+  float* zt;
+  int ldz, n, ntiles, prow;
+  long long item_end;
+};
+struct PArgs {
+  PMat mat[kMaxGroup];
+  int count, d, ngroups, ebuf_bytes, pf_items;
+  long long total;
+};
+
+__host__ __device__ constexpr int round_up16(int b) { return (b + 15) & ~15; }
+
+template <typename Tin>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int CPL = 4;
+  __device__ __forceinline__ static void load(const float* p, float (&g)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    g[0] = v.x, g[1] = v.y, g[2] = v.z, g[3] = v.w;
+  }
+};
+template <>
+struct Vec<bf16> {
+  static constexpr int CPL = 8;
+  __device__ __forceinline__ static void load(const bf16* p, float (&g)[8]) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      g[2 * t] = __uint_as_float(w[t] << 16);
+      g[2 * t + 1] = __uint_as_float(w[t] & 0xffff0000u);
+    }
+  }
+};
+
+template <typename Tin, int U>
+__global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_constant__ PArgs A) {
+  constexpr int CPL = Vec<Tin>::CPL;
+  constexpr int CT = 32 * CPL;  // columns per tile
+  constexpr int LDS = CT + 1;   // padded row of the transpose buffer
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* zs = reinterpret_cast<float*>(smem_raw);                        // [2][kBG][LDS]
+  unsigned char* ebuf = smem_raw + 2 * kBG * LDS * sizeof(float);        // [2][A.ebuf_bytes]
+  unsigned long long* ebar = reinterpret_cast<unsigned long long*>(ebuf + 2 * A.ebuf_bytes);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rot = lane / (32 / CPL);  // store rotation: conflict-free transposed writes
+
+  struct It {
+    int mi, j0, b0, elo;
+  };
+  auto item_at = [&](long long item) {
+    int mi = 0;
+    while (mi + 1 < A.count && item >= A.mat[mi].item_end) ++mi;
+    const long long lt = item - (mi ? A.mat[mi - 1].item_end : 0);
+    const int b0 = static_cast<int>(lt % A.ngroups) * kBG;
+    const int elo = __ldg(A.mat[mi].ptr + b0) & ~1;  // 16-byte aligned start
+    return It{mi, static_cast<int>(lt / A.ngroups) * CT, b0, elo};
+  };
+  // bulk-copy the CSC entries of an item's 32 bins into entry buffer `b`
+  auto stage = [&](long long item, int b) {
+    const It t = item_at(item);
+    const PMat& M = A.mat[t.mi];
+    const int ehi = __ldg(M.ptr + min(t.b0 + kBG, A.d));
+    const unsigned bytes = static_cast<unsigned>(round_up16((ehi - t.elo) * 8));
+    mbar_arrive_expect_tx(ebar + b, bytes);
+    if (bytes) bulk_load(ebuf + b * A.ebuf_bytes, M.ent + t.elo, bytes, ebar + b);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(ebar, 1);
+    mbar_init(ebar + 1, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long first = blockIdx.x;
+  if (threadIdx.x == 0) {
+    if (first < A.total) stage(first, 0);
+    if (first + gridDim.x < A.total) stage(first + gridDim.x, 1);
+  }
+  int k = 0;
+  for (long long item = first; item < A.total; item += gridDim.x, ++k) {
+    const int buf = k & 1;
+    const It t = item_at(item);
+    const PMat& M = A.mat[t.mi];
+    const int jl = t.j0 + lane * CPL;
+    const bool col_ok = jl < M.n;
+    const Tin* gcol = static_cast<const Tin*>(M.g) + jl;
+    const EntryF* es = reinterpret_cast<const EntryF*>(ebuf + buf * A.ebuf_bytes) - t.elo;
+    if (A.pf_items && threadIdx.x == 32) {
+      // first touches of G from HBM, a few column tiles ahead: item (t', g)
+      // prefetches row slice g of tile t', so the r re-reads hit L2
+      const long long f = item + A.pf_items;
+      if (f < A.total) {
+        const It tf = item_at(f);
+        const PMat& F = A.mat[tf.mi];
+        tma_prefetch_2d(&F.tmap, tf.j0, (tf.b0 / kBG) * F.prow);
+      }
+    }
+    float* z = zs + buf * kBG * LDS;
+    mbar_wait(ebar + buf, (k >> 1) & 1);
+
+    // this warp's two bins as one entry stream [bin A | bin B], U loads in
+    // flight, the next batch issued before the current one is consumed
+    const int bA = t.b0 + warp, bB = t.b0 + warp + kSWarps;
+    const int eA0 = bA < A.d ? __ldg(M.ptr + bA) : 0, eA1 = bA < A.d ? __ldg(M.ptr + bA + 1) : 0;
+    const int eB0 = bB < A.d ? __ldg(M.ptr + bB) : 0, eB1 = bB < A.d ? __ldg(M.ptr + bB + 1) : 0;
+    const int nA = eA1 - eA0, T = nA + (eB1 - eB0);
+    float acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    auto flush = [&](int bb) {
+      // z[bb][lane*CPL + c], components rotated per lane group so that the
+      // CPL stores of a warp each hit 32 distinct banks
+      float* zr = z + bb * LDS + lane * CPL;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int cc = (c + rot) % CPL;
+        float v = acc[0];
+#pragma unroll
+        for (int q = 1; q < CPL; ++q)
+          if (cc == q) v = acc[q];
+        zr[cc] = v;
+      }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    };
+    float ga[U][CPL], gb[U][CPL], pa[U], pb[U];
+    auto load = [&](int t0, float (&g)[U][CPL], float (&p)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tt = t0 + u;
+        p[u] = 0.0f;
+        if (tt < T) {
+          const uint2 en = *reinterpret_cast<const uint2*>(es + (tt < nA ? eA0 + tt : eB0 + tt - nA));
+          p[u] = __uint_as_float(en.y);
+          if (col_ok) Vec<Tin>::load(gcol + static_cast<long long>(static_cast<int>(en.x)) * M.ldg, g[u]);
+        }
+      }
+    };
+    auto consume = [&](int t0, const float (&g)[U][CPL], const float (&p)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tt = t0 + u;
+        if (tt < T) {
+          if (tt == nA) flush(warp);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p[u], g[u][c], acc[c]);
+        }
+      }
+    };
+    if (T > 0) load(0, ga, pa);
+    for (int t0 = 0; t0 < T; t0 += 2 * U) {
+      if (t0 + U < T) load(t0 + U, gb, pb);
+      consume(t0, ga, pa);
+      if (t0 + U >= T) break;
+      if (t0 + 2 * U < T) load(t0 + 2 * U, ga, pa);
+      consume(t0 + U, gb, pb);
+    }
+    if (T == nA) flush(warp);  // bin B empty (or both): bin A not flushed yet
+    flush(warp + kSWarps);
+    __syncthreads();  // z[buf] complete; entry buffer `buf` free
+    if (threadIdx.x == 0 && item + 2 * gridDim.x < A.total) stage(item + 2 * gridDim.x, buf);
+    // Z^T[j0 + c][b0 + lane]: one 128-byte row segment per column
+    const bool bin_ok = t.b0 + lane < A.d;
+    for (int c = warp; c < CT; c += kSWarps) {
+      const int j = t.j0 + c;
+      if (j < M.n && bin_ok)
+        M.zt[static_cast<long long>(j) * M.ldz + t.b0 + lane] = z[lane * LDS + c];
+    }
+    // z[buf] is rewritten two items later, after the next __syncthreads
+  }
+}
+
+template <typename Tin>
+bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
+  constexpr int CPL = Vec<Tin>::CPL;
+  constexpr int CT = 32 * CPL;
+  const Pair& p0 = *jobs[0].pr;
+  PArgs A{};
+  A.count = static_cast<int>(jobs.size());
+  A.d = p0.d;
+  A.ngroups = ceil_div(p0.d, kBG);
+  long long total = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const S1Job& J = jobs[i];
+    const Pair& pr = *J.pr;
+    // 16-byte row segments: G aligned, columns and leading dimension in whole vectors
+    if (reinterpret_cast<uintptr_t>(J.g) % 16 || pr.n % CPL || J.ldg % CPL) return false;
+    PMat& M = A.mat[i];
+    M.g = J.g;
+    M.ldg = J.ldg;
+    M.ptr = pr.p->csc_ptr.as<int>();
+    M.ent = pr.p->csc_entries();
+    M.zt = static_cast<float*>(J.zt);
+    M.ldz = pr.ldz();
+    M.n = pr.n;
+    M.ntiles = ceil_div(pr.n, CT);
+    M.prow = ceil_div(pr.m, A.ngroups);
+    if (M.prow > 256 || !cached_tmap(&M.tmap, J.g, std::is_same<Tin, float>::value ? LSP_F32 : LSP_BF16,
+                                      pr.m, pr.n, J.ldg, CT, M.prow))
+      M.prow = 0;
+    total += static_cast<long long>(M.ntiles) * A.ngroups;
+    M.item_end = total;
+  }
+  A.total = total;
+  if (total == 0) return true;
+  int pf_tiles = 8;  // L2 prefetch distance in column tiles (env LSP_SPMM_PF, 0 = off)
+  if (const char* e = std::getenv("LSP_SPMM_PF")) pf_tiles = std::atoi(e);
+  for (int i = 0; i < A.count; ++i)
+    if (A.mat[i].prow == 0) pf_tiles = 0;
+  A.pf_items = pf_tiles * A.ngroups;
+  // entry buffer: the largest 32-bin CSC range of any matrix (+16 B alignment slack)
+  int emax = 0;
+  for (const S1Job& J : jobs) {
+    const std::vector<int32_t>& ptr = J.pr->p->h_csc_ptr;
+    for (int b0 = 0; b0 < p0.d; b0 += kBG)
+      emax = std::max(emax, ptr[std::min(b0 + kBG, p0.d)] - (ptr[b0] & ~1));
+  }
+  A.ebuf_bytes = round_up16(emax * 8 + 16);
+  const int smem = 2 * kBG * (CT + 1) * static_cast<int>(sizeof(float)) + 2 * A.ebuf_bytes + 16;
+  if (smem > 227 * 1024) return false;
+  auto kern = k_compress_spmm<Tin, 32 / CPL>;
+  LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
+  kern<<<grid, kSThreads, smem, st>>>(A);
+  after_launch("compress_spmm");
+  return true;
+}
+
+}  // namespace
+
+// Gather-form stage 1 (fp32 accumulation, fp32/bf16 G); false when the group
+// is not eligible or LSP_COMPRESS_SPMM is not 1.
+bool launch_compress_spmm_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, cudaStream_t st) {
+  if (jobs.empty()) return false;
+  // opt-in (LSP_COMPRESS_SPMM=1) until it beats the fixed-slot kernel
+  const char* env = std::getenv("LSP_COMPRESS_SPMM");
+  if (!env || env[0] != '1') return false;
+  const char* gen = std::getenv("LSP_COMPRESS_GENERIC");
+  if (gen && gen[0] == '1') return false;
+  const Pair& p0 = *jobs[0].pr;
+  if (p0.compute != LSP_F32) return false;
+  if (gdt == LSP_F32) return spmm_impl<float>(jobs, st);
+  if (gdt == LSP_BF16) return spmm_impl<bf16>(jobs, st);
+  return false;
+}
+
+}  // namespace lspb

@@ -106,6 +106,10 @@ struct Projector {
   // CSR positions multiplied by `scale` (cached per scale), for kernels that
   // index shared-memory rows by byte offset.
   const int* scaled_pos(int scale);
+  // CSC entries packed as {row, value} (fp32 compute only), built on first use
+  // and kept current by refresh_values.
+  const EntryF* csc_entries();
+  DevBuf csc_ent;
   std::vector<std::pair<int, std::unique_ptr<DevBuf>>> scaled;
   // Re-derive CSC and chunk-table values from the CSR values on the device.
   void refresh_values(cudaStream_t st);
@@ -122,6 +126,8 @@ struct Pair {
   DevBuf d_t;   // d x d,  compute    (delta^T or transposed input)
   DevBuf red;   // double partial sums
   DevBuf flag;  // int
+  mutable DevBuf yb;  // float [nbands][d][BN]: Y = delta Q^T, band-blocked (apply.cu)
+  void yb_ensure(size_t bytes) const { yb.ensure(bytes); }
   int ldz() const { return static_cast<int>(round_up(d, 4)); }
   int* flag_ptr();
 };
@@ -167,6 +173,8 @@ void launch_compress_stage1_group(const std::vector<S1Job>& jobs, lsp_dtype gdt,
                                   cudaStream_t st);
 // Fixed-slot TMA variant (compress_slots.cu); false if the group is not eligible.
 bool launch_compress_slots_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, cudaStream_t st);
+// Gather-form kernel (compress_spmm.cu); false if the group is not eligible.
+bool launch_compress_spmm_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, cudaStream_t st);
 void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t st);
 void compress_group_T(const std::vector<S1Job>& jobs, lsp_dtype gdt, int* flag,
                       cudaStream_t st);
@@ -185,6 +193,9 @@ void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long
 // TMA/mbarrier fast path; returns false when the shapes or pointers do not allow it.
 bool launch_decompress_group_tma(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                                  double beta, const int* skip_flag, cudaStream_t st);
+// Y-precompute + streaming apply (apply.cu); false when not eligible.
+bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
+                               double beta, const int* skip_flag, cudaStream_t st);
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st);

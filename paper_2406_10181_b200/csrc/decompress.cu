@@ -346,6 +346,12 @@ static bool force_generic() {
   return e && e[0] == '1';
 }
 
+// LSP_DECOMPRESS_BAND=1 skips the Y-precompute path (builds Y_band in-kernel).
+static bool force_band() {
+  const char* e = std::getenv("LSP_DECOMPRESS_BAND");
+  return e && e[0] == '1';
+}
+
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st) {
@@ -356,6 +362,9 @@ void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, doub
   for (const DecJob& J : jobs)
     require(J.pr->d == p0.d && J.pr->p->r == p0.p->r && J.pr->compute == p0.compute,
             "decompress group: matrices must share d, r and compute dtype");
+  if (!partials && !force_generic() && !force_band() &&
+      launch_decompress_group_y(jobs, dt, alpha, beta, skip_flag, st))
+    return;
   if (!partials && !force_generic() &&
       launch_decompress_group_tma(jobs, dt, alpha, beta, skip_flag, st))
     return;

@@ -229,6 +229,11 @@ void launch_refresh_values(const Projector& p, cudaStream_t st) {
       after_launch("refresh_chunks");
     }
     if constexpr (sizeof(T) == 4) {
+      if (p.csc_ent.p && nnz) {
+        k_gather_entry_values<EntryF, T><<<grid_for(nnz), 256, 0, st>>>(
+            nnz, p.csc_perm.as<int>(), p.val.as<T>(), p.csc_ent.as<EntryF>());
+        after_launch("refresh_csc_entries");
+      }
       for (const auto& t : p.slot_tables) {
         k_gather_entry_values<EntryF, T><<<grid_for(t->nslots), 256, 0, st>>>(
             t->nslots, t->perm.as<int>(), p.val.as<T>(), t->slots.as<EntryF>());

@@ -322,21 +322,43 @@ def test_launch_count_increases(cuda, port):
     assert lsp.launch_count() >= before + 2
 
 
-@pytest.mark.parametrize("generic", ["0", "1"])
-def test_decompress_paths_agree(cuda, port, generic, monkeypatch):
-    """The TMA/mbarrier kernel and the generic cp.async kernel are bitwise identical
-    and both match the oracle (incl. ragged m, n and the group tile split)."""
-    monkeypatch.setenv("LSP_DECOMPRESS_GENERIC", generic)
-    for (m, n, d) in [(777, 1000, 64), (130, 4100, 128), (4096, 96, 256)]:
-        P, Q, pair = make(port, m, n, d, 4, m + n)
+@pytest.mark.parametrize("path", ["y", "band", "generic"])
+def test_decompress_paths_agree(cuda, port, path, monkeypatch):
+    """The Y-precompute streaming kernel (apply.cu), the in-kernel Y_band TMA kernel
+    and the generic cp.async kernel match the oracle (incl. ragged m, n, d not a
+    multiple of 64, r = 8, wide d -> narrower bands, and the group tile split)."""
+    monkeypatch.setenv("LSP_DECOMPRESS_GENERIC", "1" if path == "generic" else "0")
+    monkeypatch.setenv("LSP_DECOMPRESS_BAND", "1" if path == "band" else "0")
+    for (m, n, d, r) in [(777, 1000, 64, 4), (130, 4100, 128, 4), (4096, 96, 256, 4),
+                         (300, 517, 100, 4), (513, 700, 96, 8), (200, 300, 2048, 4),
+                         (100, 90, 4096, 4)]:
+        P, Q, pair = make(port, m, n, d, r, m + n)
         delta = f32normal(d, (d, d))
         w0 = f32normal(n, (m, n), 0.02)
         w = dev(w0)
         pair.decompress_apply(dev(delta), 1e-3, w)
         ref = port.decompress_apply(P, Q, delta, 1e-3, w0)
-        assert rel(host(w) - w0, ref - w0) < 1e-5
+        assert rel(host(w) - w0, ref - w0) < 1e-5, (m, n, d, r)
         out = host(pair.decompress(dev(delta)))
-        assert rel(out, port.decompress(P, Q, delta)) < 1e-5
+        assert rel(out, port.decompress(P, Q, delta)) < 1e-5, (m, n, d, r)
+
+
+def test_decompress_y_bitwise_vs_band(cuda, port, monkeypatch):
+    """Same arithmetic and summation order: the Y-precompute path is bitwise equal
+    to the in-kernel Y_band kernel, for fp32 and bf16 W."""
+    m, n, d = 1000, 1500, 256
+    P, Q, pair = make(port, m, n, d, 4, 7)
+    delta = dev(f32normal(d, (d, d)))
+    for wdt in (torch.float32, torch.bfloat16):
+        w0 = (0.02 * torch.randn(m, n, device="cuda")).to(wdt)
+        outs = []
+        for band in ("0", "1"):
+            monkeypatch.setenv("LSP_DECOMPRESS_BAND", band)
+            w = w0.clone()
+            pair.decompress_apply(delta, 1e-3, w)
+            outs.append(w)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1])
 
 
 def _skewed(m, d, r, seed, hot):
@@ -355,33 +377,38 @@ def _skewed(m, d, r, seed, hot):
 @pytest.mark.parametrize("pin", ["", "1,2", "1,4", "1,8", "2,2", "2,4"])
 @pytest.mark.parametrize("gdt", ["f32", "bf16"])
 def test_compress_paths_agree(cuda, port, gdt, pin, monkeypatch):
-    """Fixed-slot TMA stage 1 vs the CSC-walk stage 1: bitwise identical (same
-    per-bin summation order), both on the oracle; random and skewed projectors,
-    ragged m and n, d not a multiple of 32; every (columns per lane, K) variant."""
+    """Gather-form stage 1 (compress_spmm.cu), fixed-slot TMA stage 1 and the
+    CSC-walk stage 1: bitwise identical (same per-bin summation order), all on
+    the oracle; random and skewed projectors, ragged m and n, d not a multiple
+    of 32; every (columns per lane, K) variant of the slot kernel."""
     monkeypatch.setenv("LSP_COMPRESS_SLOTS", pin)
     cases = []
     for (m, n, d, r) in [(777, 1000, 64, 4), (1300, 4100, 128, 4), (4096, 96, 1024, 4),
-                         (513, 257, 100, 3), (2000, 300, 2048, 4)]:
+                         (513, 257, 100, 3), (2000, 300, 2048, 4), (300, 8192, 64, 4)]:
         P, Q, _ = make(port, m, n, d, r, m + n)
         cases.append((P, Q))
     for hot in (1, 3):
-        cases.append((_skewed(1500, 96, 4, hot, hot), port.init_sparse(700, 96, 4, 5)))
+        cases.append((_skewed(1500, 96, 4, hot, hot), port.init_sparse(704, 96, 4, 5)))
     for P, Q in cases:
         g = f32normal(P.n_rows, (P.n_rows, Q.n_rows))
         if gdt == "bf16":
             g = bf16_round(g)
         outs = []
-        for generic in ("0", "1"):
+        for spmm, generic in (("1", "0"), ("0", "0"), ("0", "1")):
+            monkeypatch.setenv("LSP_COMPRESS_SPMM", spmm)
             monkeypatch.setenv("LSP_COMPRESS_GENERIC", generic)
             pair = lsp.DevicePair(lsp.DeviceProjector(P.n_rows, P.d, P.r, P.pos, P.val),
                                   lsp.DeviceProjector(Q.n_rows, Q.d, Q.r, Q.pos, Q.val))
             outs.append(pair.compress(dev(g, gdt)).clone())
-        assert torch.equal(outs[0], outs[1])
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
         assert rel(host(outs[0]), port.compress(P, Q, g)) < 1e-5
 
 
-def test_compress_slots_value_refresh(cuda, port):
-    """set_values re-derives the slot and overflow tables' values on the device."""
+@pytest.mark.parametrize("spmm", ["1", "0"])
+def test_compress_slots_value_refresh(cuda, port, spmm, monkeypatch):
+    """set_values re-derives the slot/overflow tables' and the packed CSC entries'
+    values on the device (gather kernel and slot kernel)."""
+    monkeypatch.setenv("LSP_COMPRESS_SPMM", spmm)
     P = _skewed(900, 64, 4, 11, 2)
     Q = port.init_sparse(300, 64, 4, 12)
     dp = lsp.DeviceProjector(P.n_rows, P.d, P.r, P.pos, P.val)
