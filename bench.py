@@ -291,7 +291,7 @@ def run_ours(args):
     from paper_2406_10181_b200.schedule import LayerSchedule
 
     ev = {(ph, li): (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for ph in ("compress", "adam", "apply") for li in range(L)}
+          for ph in ("compress", "adam", "build", "apply") for li in range(L)}
     recording = [False]
 
     def record(ph, li, when):
@@ -335,6 +335,10 @@ def run_ours(args):
     comp_ms = [ev[("compress", li)][0].elapsed_time(ev[("compress", li)][1]) for li in range(L)]
     adam_ms = [ev[("adam", li)][0].elapsed_time(ev[("adam", li)][1]) for li in range(L)]
     app_ms = [ev[("apply", li)][0].elapsed_time(ev[("apply", li)][1]) for li in range(L)]
+    try:
+        build_ms = [ev[("build", li)][0].elapsed_time(ev[("build", li)][1]) for li in range(L)]
+    except RuntimeError:  # layer without a split apply
+        build_ms = [0.0] * L
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -355,7 +359,7 @@ def run_ours(args):
     comp_avg = float(np.mean(comp_ms))
     app_ach = app_bytes / (app_avg * 1e-3) / 1e9
     comp_ach = comp_bytes / (comp_avg * 1e-3) / 1e9
-    tsum = sum(app_ms) + sum(comp_ms) + sum(adam_ms)
+    tsum = sum(app_ms) + sum(comp_ms) + sum(adam_ms) + sum(build_ms)
     line = {
         "metric": "grad GB/s (compress+decompress+apply)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -372,13 +376,15 @@ def run_ours(args):
                    "step_hbm_bytes_alg": balg,
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},
-        "roofline": {"kernel": "k_decompress_band (grouped fused decompress-and-apply, 1 launch "
-                               "per layer)",
+        "roofline": {"kernel": "k_apply_y (grouped streaming decompress-and-apply W -= lr P Y, "
+                               "1 launch per layer; Y = delta Q^T built by k_build_y_smem just "
+                               "before, timed separately as build_ms)",
                      "bound": "hbm", "achieved": app_ach, "peak": peak, "unit": "GB/s",
                      "frac": app_ach / peak, "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch_avg": app_bytes, "avg_launch_ms": app_avg,
                      "share_of_step": sum(app_ms) / (ms if ms > 0 else 1)},
         "breakdown": {"compress_ms_per_step": sum(comp_ms), "adam_ms_per_step": sum(adam_ms),
+                      "build_y_ms_per_step": sum(build_ms),
                       "apply_ms_per_step": sum(app_ms), "other_ms_per_step": ms - tsum,
                       "compress_achieved_gbs": comp_ach, "compress_frac": comp_ach / peak,
                       "apply_achieved_gbs": app_ach},

@@ -247,6 +247,14 @@ int lsp_layer_update(lsp_layer_t layer, double lr, int check_finite, lsp_stream_
 int lsp_layer_adam(lsp_layer_t layer, int check_finite, lsp_stream_t stream);
 int lsp_layer_apply(lsp_layer_t layer, double lr, lsp_stream_t stream);
 /* compress + update. */
+/* lsp_layer_apply in two enqueued halves (same stream, in this order): the
+ * Y = delta Q^T build of every matrix, then the streaming apply that reads it.
+ * For groups the Y path does not cover, _prepare enqueues nothing and _finish
+ * runs the whole apply.  Lets a caller time or overlap the halves.
+ * Replaces: decompress (rightT_mul then left_mul) + apply, proj/src/projector.cpp:170-175,
+ * proj/src/trainer.cpp:190. */
+int lsp_layer_apply_prepare(lsp_layer_t layer, lsp_stream_t stream);
+int lsp_layer_apply_finish(lsp_layer_t layer, double lr, lsp_stream_t stream);
 int lsp_layer_step(lsp_layer_t layer, double lr, lsp_stream_t stream);
 /* SYNCHRONOUS: LSP_ENUMERIC if a non-finite S was seen (clears the flag). */
 int lsp_layer_check(lsp_layer_t layer, lsp_stream_t stream);

@@ -114,6 +114,8 @@ _SIGS = {
     "lsp_layer_update": (_i, [_vp, _d, _i, _vp]),
     "lsp_layer_adam": (_i, [_vp, _i, _vp]),
     "lsp_layer_apply": (_i, [_vp, _d, _vp]),
+    "lsp_layer_apply_prepare": (_i, [_vp, _vp]),
+    "lsp_layer_apply_finish": (_i, [_vp, _d, _vp]),
     "lsp_layer_step": (_i, [_vp, _d, _vp]),
     "lsp_layer_check": (_i, [_vp, _vp]),
     "lsp_layer_adam_get": (_i, [_vp, _i, _dp, _dp, C.POINTER(_i64), _i]),

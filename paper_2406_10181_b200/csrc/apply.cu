@@ -156,17 +156,46 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_c
   int4* epos = reinterpret_cast<int4*>(ds + d * 32) + warp * 2 * NQ;  // [NQ] pos, then [NQ] val
   const long long u_begin = A.units * blockIdx.x / gridDim.x;
   const long long u_end = A.units * (blockIdx.x + 1) / gridDim.x;
-  int cur_mi = -1, cur_ab = -1;
-  for (long long u = u_begin; u < u_end; ++u) {
+  struct UInfo {
+    int mi, ab, chunk, band_end;
+  };
+  auto decode = [&](long long u) {
     int mi = 0;
     while (mi + 1 < A.count && u >= A.mat[mi].task_end) ++mi;
     const YMat& M = A.mat[mi];
     const long long lt = u - (mi ? A.mat[mi - 1].task_end : 0);
     const int nchunks = (M.nbands + kYBands - 1) / kYBands;
-    const int ab = static_cast<int>(lt / nchunks);
     const int chunk = static_cast<int>(lt % nchunks);
-    const int a0 = ab * 32;
-    if (mi != cur_mi || ab != cur_ab) {
+    return UInfo{mi, static_cast<int>(lt / nchunks), chunk, min(M.nbands, (chunk + 1) * kYBands)};
+  };
+  // the band's BN*KR (pos, val) pairs are contiguous in the CSR arrays of Q
+  auto fetch = [&](int mi, int band, int band_end, int4 (&pr)[NE], float4 (&vr)[NE]) {
+    const YMat& F = A.mat[mi];
+    const long long qlim = static_cast<long long>(F.n) * KR;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int t = lane + 32 * e;
+      const long long off = static_cast<long long>(band) * BN * KR + 4LL * t;
+      pr[e] = make_int4(0, 0, 0, 0);
+      vr[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < NQ && band < band_end && off < qlim) {
+        pr[e] = __ldg(reinterpret_cast<const int4*>(F.qpos + off));
+        vr[e] = __ldg(reinterpret_cast<const float4*>(F.qval + off));
+      }
+    }
+  };
+  int4 pr[NE];
+  float4 vr[NE];
+  if (u_begin < u_end) {
+    const UInfo f = decode(u_begin);
+    fetch(f.mi, f.chunk * kYBands + warp, f.band_end, pr, vr);
+  }
+  int cur_mi = -1, cur_ab = -1;
+  for (long long u = u_begin; u < u_end; ++u) {
+    const UInfo U = decode(u);
+    const YMat& M = A.mat[U.mi];
+    const int a0 = U.ab * 32;
+    if (U.mi != cur_mi || U.ab != cur_ab) {
       __syncthreads();  // previous block fully consumed
       // ds[b][t] = Delta^T[b][a0 + t]  (zero beyond d); 8 loads in flight per thread
       for (int i0 = threadIdx.x; i0 < d * 8; i0 += 8 * blockDim.x) {
@@ -194,31 +223,16 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_c
         }
       }
       __syncthreads();
-      cur_mi = mi;
-      cur_ab = ab;
+      cur_mi = U.mi;
+      cur_ab = U.ab;
     }
     const int a = a0 + lane;
-    const int band_end = min(M.nbands, (chunk + 1) * kYBands);
-    // the band's BN*KR (pos, val) pairs are contiguous in the CSR arrays of Q
-    const long long qlim = static_cast<long long>(M.n) * KR;
-    auto fetch = [&](int band, int4 (&pr)[NE], float4 (&vr)[NE]) {
-#pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const int t = lane + 32 * e;
-        const long long off = static_cast<long long>(band) * BN * KR + 4LL * t;
-        pr[e] = make_int4(0, 0, 0, 0);
-        vr[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (t < NQ && band < band_end && off < qlim) {
-          pr[e] = __ldg(reinterpret_cast<const int4*>(M.qpos + off));
-          vr[e] = __ldg(reinterpret_cast<const float4*>(M.qval + off));
-        }
-      }
-    };
-    int4 pr[NE];
-    float4 vr[NE];
-    int band = chunk * kYBands + warp;
-    fetch(band, pr, vr);
-    for (; band < band_end; band += kYWarps) {
+    const int band0 = U.chunk * kYBands + warp;
+    if (band0 >= U.band_end && u + 1 < u_end) {  // no band here: entries for the next unit
+      const UInfo f = decode(u + 1);
+      fetch(f.mi, f.chunk * kYBands + warp, f.band_end, pr, vr);
+    }
+    for (int band = band0; band < U.band_end; band += kYWarps) {
       __syncwarp();
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
@@ -229,7 +243,14 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_c
         }
       }
       __syncwarp();
-      fetch(band + kYWarps, pr, vr);  // next band's entries in flight
+      // next band's entries in flight while this one is computed (possibly in
+      // the next unit of this CTA's range)
+      if (band + kYWarps < U.band_end) {
+        fetch(U.mi, band + kYWarps, U.band_end, pr, vr);
+      } else if (u + 1 < u_end) {
+        const UInfo f = decode(u + 1);
+        fetch(f.mi, f.chunk * kYBands + warp, f.band_end, pr, vr);
+      }
       const int* sp = reinterpret_cast<const int*>(epos);
       const float* sv = reinterpret_cast<const float*>(epos + NQ);
       float y[BN];
@@ -577,7 +598,7 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
 
 template <int BN, int KR>
 bool run_bn(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha, double beta,
-            const int* skip, cudaStream_t st) {
+            const int* skip, cudaStream_t st, int phase) {
   for (const DecJob& J : jobs) {
     const Pair& pr = *J.pr;
     J.pr->yb_ensure(static_cast<size_t>(ceil_div(pr.n, BN)) * pr.d * BN * sizeof(float));
@@ -591,9 +612,18 @@ bool run_bn(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha, double 
       const size_t es = dtype_size(dt);
       if (reinterpret_cast<uintptr_t>(J.in) % 16 || (J.ldi * es) % 16) return false;
     }
-  // Y build + apply per subgroup whose Y blocks fit comfortably in L2, so the
-  // apply reads Y from L2 rather than HBM (env LSP_APPLY_YB_MB, default 64)
-  size_t budget = 64ull << 20;
+  if (phase != kPhaseBoth) {  // split form: the whole group, build or apply
+    if (phase == kPhaseBuild) build_y_impl<BN, KR>(jobs, skip, st);
+    if (phase == kPhaseApply) {
+      const bool ok = dt == LSP_F32 ? apply_impl<float, BN, KR>(jobs, alpha, beta, skip, st)
+                                    : apply_impl<bf16, BN, KR>(jobs, alpha, beta, skip, st);
+      require(ok, "apply_y: launch configuration rejected after the Y build");
+    }
+    return true;
+  }
+  // Y build + apply per subgroup of at most LSP_APPLY_YB_MB of Y blocks
+  // (default: the whole group -- measured faster than L2-sized subgroups)
+  size_t budget = ~size_t(0);
   if (const char* e = std::getenv("LSP_APPLY_YB_MB")) budget = static_cast<size_t>(std::atoi(e)) << 20;
   size_t i = 0;
   while (i < jobs.size()) {
@@ -620,7 +650,7 @@ bool run_bn(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha, double 
 // Fast path of launch_decompress_group for fp32 accumulation, W in fp32 or
 // bf16, r in {4, 8}; false (nothing enqueued) when not eligible.
 bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
-                               double beta, const int* skip_flag, cudaStream_t st) {
+                               double beta, const int* skip_flag, cudaStream_t st, int phase) {
   if (jobs.empty() || jobs.size() > static_cast<size_t>(kMaxGroup)) return false;
   const Pair& p0 = *jobs[0].pr;
   if (p0.compute != LSP_F32 || (dt != LSP_F32 && dt != LSP_BF16)) return false;
@@ -631,8 +661,8 @@ bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, do
   const int d = p0.d;
   auto pick = [&](auto bn) -> bool {
     constexpr int BN = decltype(bn)::value;
-    return r == 4 ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st)
-                  : run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st);
+    return r == 4 ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st, phase)
+                  : run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st, phase);
   };
   const char* bn_env = std::getenv("LSP_APPLY_BN");
   const int bn_max = bn_env ? std::atoi(bn_env) : 32;

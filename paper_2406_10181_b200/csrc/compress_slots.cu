@@ -19,11 +19,13 @@
 // summation order per bin is still ascending rows, so results are bitwise
 // those of k_compress_stage1.
 //
-// Data movement: thread 0 is the producer.  Per chunk it issues ceil(bm/256)
-// 2-D TMA loads of the G tile (evict-first: G is read once) plus one 1-D bulk
-// copy of the CTA's slot block, all completing on the stage's "full"
-// mbarrier; warps arrive on the stage's "empty" mbarrier when done, and thread
-// 0 refills the stage two chunks ahead.  No block-wide barrier in the loop.
+// Data movement: per chunk, ceil(bm/256) 2-D TMA loads of the G tile
+// (evict-first: G is read once) plus one 1-D bulk copy of the CTA's slot
+// block, all completing on the stage's "full" mbarrier.  Thread 0 issues the
+// first two chunks; afterwards the LAST warp to finish a chunk (elected with a
+// shared-memory counter, after every warp arrived on the stage's "empty"
+// mbarrier) refills that stage two chunks ahead.  No block-wide barrier in the
+// loop, and the refill never waits for one particular warp.
 #include <cuda.h>
 
 #include <algorithm>
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_slots(const __grid_c
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + 2 * A.stage_bytes);
   unsigned long long* empty = full + 2;
+  unsigned* done = reinterpret_cast<unsigned*>(empty + 2);  // [2] warps finished per stage
   // the CTAs of one band (bin ranges) are adjacent in launch order: G tiles
   // are fetched from HBM once and re-read from L2
   const int gband = blockIdx.x / A.cpb;
@@ -116,6 +119,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_slots(const __grid_c
     for (int s = 0; s < 2; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, WARPS);
+      done[s] = 0u;
     }
     fence_mbar_init();
   }
@@ -208,10 +212,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_slots(const __grid_c
       mbar_wait(full + s, (c >> 1) & 1);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
-    if (tid == 0 && c + 2 < nchunks) {
-      mbar_wait(empty + s, (c >> 1) & 1);
-      issue(c + 2);
+    if (lane == 0) {
+      mbar_arrive(empty + s);
+      // the LAST warp to finish the chunk refills its stage (no coupling of
+      // the refill to one warp's progress)
+      if (c + 2 < nchunks && atomicAdd(done + s, 1u) == WARPS - 1) {
+        done[s] = 0u;
+        mbar_wait(empty + s, (c >> 1) & 1);
+        issue(c + 2);
+      }
     }
   }
   if (!active) return;

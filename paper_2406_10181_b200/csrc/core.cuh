@@ -193,9 +193,13 @@ void launch_decompress(const Pair& pr, const void* delta_t, const void* in, long
 // TMA/mbarrier fast path; returns false when the shapes or pointers do not allow it.
 bool launch_decompress_group_tma(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                                  double beta, const int* skip_flag, cudaStream_t st);
-// Y-precompute + streaming apply (apply.cu); false when not eligible.
+// Y-precompute + streaming apply (apply.cu); false when not eligible.  phase:
+// both kernels, only the Y build, or only the apply (after a Y build of the
+// same group on the same stream).
+constexpr int kPhaseBuild = 1, kPhaseApply = 2, kPhaseBoth = 3;
 bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
-                               double beta, const int* skip_flag, cudaStream_t st);
+                               double beta, const int* skip_flag, cudaStream_t st,
+                               int phase = kPhaseBoth);
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st);

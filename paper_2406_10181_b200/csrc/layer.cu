@@ -32,6 +32,7 @@ struct lsp_layer_s {
     lsp_dtype wdt = LSP_F32;
   };
   std::vector<Bind> binds;
+  bool prepared = false;  // Y of the split apply built (lsp_layer_apply_prepare)
 
   size_t dd() const { return static_cast<size_t>(d) * d; }
   size_t vs() const { return lspb::dtype_size(compute); }
@@ -88,6 +89,33 @@ void layer_apply(lsp_layer_s& L, double lr, cudaStream_t st) {
     jobs.push_back(DecJob{L.pairs[i], L.d_block(i), L.binds[i].w, L.binds[i].ldw, L.binds[i].w,
                           L.binds[i].ldw});
   launch_decompress_group(jobs, L.binds[0].wdt, -lr, 1.0, flag, nullptr, nullptr, st);
+}
+
+std::vector<DecJob> apply_jobs(lsp_layer_s& L) {
+  std::vector<DecJob> jobs;
+  for (int i = 0; i < L.count; ++i)
+    jobs.push_back(DecJob{L.pairs[i], L.d_block(i), L.binds[i].w, L.binds[i].ldw, L.binds[i].w,
+                          L.binds[i].ldw});
+  return jobs;
+}
+
+void layer_apply_prepare(lsp_layer_s& L, cudaStream_t st) {
+  check_bound(L);
+  L.prepared = !std::getenv("LSP_DECOMPRESS_GENERIC") && !std::getenv("LSP_DECOMPRESS_BAND") &&
+               launch_decompress_group_y(apply_jobs(L), L.binds[0].wdt, -1.0, 1.0,
+                                         L.adam.flag.as<int>(), st, kPhaseBuild);
+}
+
+void layer_apply_finish(lsp_layer_s& L, double lr, cudaStream_t st) {
+  check_bound(L);
+  if (L.prepared) {
+    L.prepared = false;
+    require(launch_decompress_group_y(apply_jobs(L), L.binds[0].wdt, -lr, 1.0,
+                                      L.adam.flag.as<int>(), st, kPhaseApply),
+            "layer_apply_finish: apply rejected after the Y build");
+    return;
+  }
+  layer_apply(L, lr, st);
 }
 
 void layer_update(lsp_layer_s& L, double lr, bool check, cudaStream_t st) {
@@ -204,6 +232,20 @@ int lsp_layer_apply(lsp_layer_t L, double lr, lsp_stream_t stream) {
   return guard_layer([&] {
     require(L != nullptr, "layer_apply: null layer");
     layer_apply(*L, lr, as_stream(stream));
+  });
+}
+
+int lsp_layer_apply_prepare(lsp_layer_t L, lsp_stream_t stream) {
+  return guard_layer([&] {
+    require(L != nullptr, "layer_apply_prepare: null layer");
+    layer_apply_prepare(*L, as_stream(stream));
+  });
+}
+
+int lsp_layer_apply_finish(lsp_layer_t L, double lr, lsp_stream_t stream) {
+  return guard_layer([&] {
+    require(L != nullptr, "layer_apply_finish: null layer");
+    layer_apply_finish(*L, lr, as_stream(stream));
   });
 }
 

@@ -450,6 +450,16 @@ class Layer:
     def apply(self, lr: float, stream=None):
         lib.layer_apply(self._h, float(lr), _stream(stream))
 
+    def apply_prepare(self, stream=None):
+        """First half of apply(): enqueue the Y = delta Q^T build (no-op for groups
+        the Y path does not cover)."""
+        lib.layer_apply_prepare(self._h, _stream(stream))
+
+    def apply_finish(self, lr: float, stream=None):
+        """Second half of apply(): the streaming W update (the whole apply if
+        apply_prepare enqueued nothing)."""
+        lib.layer_apply_finish(self._h, float(lr), _stream(stream))
+
     def step(self, lr: float, stream=None):
         lib.layer_step(self._h, float(lr), _stream(stream))
 

@@ -60,9 +60,18 @@ class LayerSchedule:
         self._rec("adam", li, "begin")
         self.layers[li].adam(self.world > 1)  # re-check finiteness after the reduction
         self._rec("adam", li, "end")
-        self._rec("apply", li, "begin")
-        self.layers[li].apply(self.lr)
-        self._rec("apply", li, "end")
+        lay = self.layers[li]
+        if hasattr(lay, "apply_prepare"):
+            self._rec("build", li, "begin")
+            lay.apply_prepare()
+            self._rec("build", li, "end")
+            self._rec("apply", li, "begin")
+            lay.apply_finish(self.lr)
+            self._rec("apply", li, "end")
+        else:
+            self._rec("apply", li, "begin")
+            lay.apply(self.lr)
+            self._rec("apply", li, "end")
 
     def order(self):
         return list(reversed(range(len(self.layers))))
