@@ -90,6 +90,80 @@ __device__ __forceinline__ void fma_bin(float (&acc)[32], int b, float v, const 
   for (int c = 0; c < CPL; ++c) acc[b * CPL + c] = fmaf(v, g[c], acc[b * CPL + c]);
 }
 
+// acc[b*CPL + c] += v * g[c] for a warp-uniform runtime bin b < 32/CPL: one
+// indirect branch (brx.idx jump table) instead of a compiler-built search tree.
+// fma.rn.f32 is exactly fmaf, so results match the unrolled slot FMAs bitwise.
+template <int CPL>
+__device__ __forceinline__ void fma_bin_dyn(float (&acc)[32], int b, float v, const float (&g)[CPL]);
+template <>
+__device__ __forceinline__ void fma_bin_dyn<1>(float (&acc)[32], int b, float v, const float (&g)[1]) {
+  asm volatile(
+      "{\n"
+      "ts%=: .branchtargets c0%=, c1%=, c2%=, c3%=, c4%=, c5%=, c6%=, c7%=, c8%=, c9%=, c10%=, c11%=, c12%=, c13%=, c14%=, c15%=, c16%=, c17%=, c18%=, c19%=, c20%=, c21%=, c22%=, c23%=, c24%=, c25%=, c26%=, c27%=, c28%=, c29%=, c30%=, c31%=;\n"
+      "brx.idx.uni %32, ts%=;\n"
+      "c0%=: fma.rn.f32 %0, %33, %34, %0; bra.uni e%=;\n"
+      "c1%=: fma.rn.f32 %1, %33, %34, %1; bra.uni e%=;\n"
+      "c2%=: fma.rn.f32 %2, %33, %34, %2; bra.uni e%=;\n"
+      "c3%=: fma.rn.f32 %3, %33, %34, %3; bra.uni e%=;\n"
+      "c4%=: fma.rn.f32 %4, %33, %34, %4; bra.uni e%=;\n"
+      "c5%=: fma.rn.f32 %5, %33, %34, %5; bra.uni e%=;\n"
+      "c6%=: fma.rn.f32 %6, %33, %34, %6; bra.uni e%=;\n"
+      "c7%=: fma.rn.f32 %7, %33, %34, %7; bra.uni e%=;\n"
+      "c8%=: fma.rn.f32 %8, %33, %34, %8; bra.uni e%=;\n"
+      "c9%=: fma.rn.f32 %9, %33, %34, %9; bra.uni e%=;\n"
+      "c10%=: fma.rn.f32 %10, %33, %34, %10; bra.uni e%=;\n"
+      "c11%=: fma.rn.f32 %11, %33, %34, %11; bra.uni e%=;\n"
+      "c12%=: fma.rn.f32 %12, %33, %34, %12; bra.uni e%=;\n"
+      "c13%=: fma.rn.f32 %13, %33, %34, %13; bra.uni e%=;\n"
+      "c14%=: fma.rn.f32 %14, %33, %34, %14; bra.uni e%=;\n"
+      "c15%=: fma.rn.f32 %15, %33, %34, %15; bra.uni e%=;\n"
+      "c16%=: fma.rn.f32 %16, %33, %34, %16; bra.uni e%=;\n"
+      "c17%=: fma.rn.f32 %17, %33, %34, %17; bra.uni e%=;\n"
+      "c18%=: fma.rn.f32 %18, %33, %34, %18; bra.uni e%=;\n"
+      "c19%=: fma.rn.f32 %19, %33, %34, %19; bra.uni e%=;\n"
+      "c20%=: fma.rn.f32 %20, %33, %34, %20; bra.uni e%=;\n"
+      "c21%=: fma.rn.f32 %21, %33, %34, %21; bra.uni e%=;\n"
+      "c22%=: fma.rn.f32 %22, %33, %34, %22; bra.uni e%=;\n"
+      "c23%=: fma.rn.f32 %23, %33, %34, %23; bra.uni e%=;\n"
+      "c24%=: fma.rn.f32 %24, %33, %34, %24; bra.uni e%=;\n"
+      "c25%=: fma.rn.f32 %25, %33, %34, %25; bra.uni e%=;\n"
+      "c26%=: fma.rn.f32 %26, %33, %34, %26; bra.uni e%=;\n"
+      "c27%=: fma.rn.f32 %27, %33, %34, %27; bra.uni e%=;\n"
+      "c28%=: fma.rn.f32 %28, %33, %34, %28; bra.uni e%=;\n"
+      "c29%=: fma.rn.f32 %29, %33, %34, %29; bra.uni e%=;\n"
+      "c30%=: fma.rn.f32 %30, %33, %34, %30; bra.uni e%=;\n"
+      "c31%=: fma.rn.f32 %31, %33, %34, %31;\n"
+      "e%=:\n}\n"
+      : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3]), "+f"(acc[4]), "+f"(acc[5]), "+f"(acc[6]), "+f"(acc[7]), "+f"(acc[8]), "+f"(acc[9]), "+f"(acc[10]), "+f"(acc[11]), "+f"(acc[12]), "+f"(acc[13]), "+f"(acc[14]), "+f"(acc[15]), "+f"(acc[16]), "+f"(acc[17]), "+f"(acc[18]), "+f"(acc[19]), "+f"(acc[20]), "+f"(acc[21]), "+f"(acc[22]), "+f"(acc[23]), "+f"(acc[24]), "+f"(acc[25]), "+f"(acc[26]), "+f"(acc[27]), "+f"(acc[28]), "+f"(acc[29]), "+f"(acc[30]), "+f"(acc[31])
+      : "r"(b), "f"(v), "f"(g[0]));
+}
+template <>
+__device__ __forceinline__ void fma_bin_dyn<2>(float (&acc)[32], int b, float v, const float (&g)[2]) {
+  asm volatile(
+      "{\n"
+      "ts%=: .branchtargets c0%=, c1%=, c2%=, c3%=, c4%=, c5%=, c6%=, c7%=, c8%=, c9%=, c10%=, c11%=, c12%=, c13%=, c14%=, c15%=;\n"
+      "brx.idx.uni %32, ts%=;\n"
+      "c0%=: fma.rn.f32 %0, %33, %34, %0; fma.rn.f32 %1, %33, %35, %1; bra.uni e%=;\n"
+      "c1%=: fma.rn.f32 %2, %33, %34, %2; fma.rn.f32 %3, %33, %35, %3; bra.uni e%=;\n"
+      "c2%=: fma.rn.f32 %4, %33, %34, %4; fma.rn.f32 %5, %33, %35, %5; bra.uni e%=;\n"
+      "c3%=: fma.rn.f32 %6, %33, %34, %6; fma.rn.f32 %7, %33, %35, %7; bra.uni e%=;\n"
+      "c4%=: fma.rn.f32 %8, %33, %34, %8; fma.rn.f32 %9, %33, %35, %9; bra.uni e%=;\n"
+      "c5%=: fma.rn.f32 %10, %33, %34, %10; fma.rn.f32 %11, %33, %35, %11; bra.uni e%=;\n"
+      "c6%=: fma.rn.f32 %12, %33, %34, %12; fma.rn.f32 %13, %33, %35, %13; bra.uni e%=;\n"
+      "c7%=: fma.rn.f32 %14, %33, %34, %14; fma.rn.f32 %15, %33, %35, %15; bra.uni e%=;\n"
+      "c8%=: fma.rn.f32 %16, %33, %34, %16; fma.rn.f32 %17, %33, %35, %17; bra.uni e%=;\n"
+      "c9%=: fma.rn.f32 %18, %33, %34, %18; fma.rn.f32 %19, %33, %35, %19; bra.uni e%=;\n"
+      "c10%=: fma.rn.f32 %20, %33, %34, %20; fma.rn.f32 %21, %33, %35, %21; bra.uni e%=;\n"
+      "c11%=: fma.rn.f32 %22, %33, %34, %22; fma.rn.f32 %23, %33, %35, %23; bra.uni e%=;\n"
+      "c12%=: fma.rn.f32 %24, %33, %34, %24; fma.rn.f32 %25, %33, %35, %25; bra.uni e%=;\n"
+      "c13%=: fma.rn.f32 %26, %33, %34, %26; fma.rn.f32 %27, %33, %35, %27; bra.uni e%=;\n"
+      "c14%=: fma.rn.f32 %28, %33, %34, %28; fma.rn.f32 %29, %33, %35, %29; bra.uni e%=;\n"
+      "c15%=: fma.rn.f32 %30, %33, %34, %30; fma.rn.f32 %31, %33, %35, %31;\n"
+      "e%=:\n}\n"
+      : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3]), "+f"(acc[4]), "+f"(acc[5]), "+f"(acc[6]), "+f"(acc[7]), "+f"(acc[8]), "+f"(acc[9]), "+f"(acc[10]), "+f"(acc[11]), "+f"(acc[12]), "+f"(acc[13]), "+f"(acc[14]), "+f"(acc[15]), "+f"(acc[16]), "+f"(acc[17]), "+f"(acc[18]), "+f"(acc[19]), "+f"(acc[20]), "+f"(acc[21]), "+f"(acc[22]), "+f"(acc[23]), "+f"(acc[24]), "+f"(acc[25]), "+f"(acc[26]), "+f"(acc[27]), "+f"(acc[28]), "+f"(acc[29]), "+f"(acc[30]), "+f"(acc[31])
+      : "r"(b), "f"(v), "f"(g[0]), "f"(g[1]));
+}
+
 template <typename Tin, int K, int CPL, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_slots(const __grid_constant__ SArgs A) {
   constexpr int BPW = 32 / CPL;  // bins per warp (32 accumulators per lane)
@@ -191,21 +265,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_slots(const __grid_c
           const float v = __uint_as_float(__shfl_sync(0xffffffffu, mine.y, t));
           float g[CPL];
           lds_g<Tin, CPL>(tl + (pk & 0x7ffffffu), g);
-          const int bin = static_cast<int>(pk >> 27);
-          // warp-uniform bin -> register: a compiler-built branch tree
-#define LSP_CASE(q) \
-  case q:           \
-    if (q < BPW) fma_bin<CPL>(acc, q < BPW ? q : 0, v, g); \
-    break;
-          switch (bin) {
-            LSP_CASE(0) LSP_CASE(1) LSP_CASE(2) LSP_CASE(3) LSP_CASE(4) LSP_CASE(5)
-            LSP_CASE(6) LSP_CASE(7) LSP_CASE(8) LSP_CASE(9) LSP_CASE(10) LSP_CASE(11)
-            LSP_CASE(12) LSP_CASE(13) LSP_CASE(14) LSP_CASE(15) LSP_CASE(16) LSP_CASE(17)
-            LSP_CASE(18) LSP_CASE(19) LSP_CASE(20) LSP_CASE(21) LSP_CASE(22) LSP_CASE(23)
-            LSP_CASE(24) LSP_CASE(25) LSP_CASE(26) LSP_CASE(27) LSP_CASE(28) LSP_CASE(29)
-            LSP_CASE(30) LSP_CASE(31)
-          }
-#undef LSP_CASE
+          fma_bin_dyn<CPL>(acc, static_cast<int>(pk >> 27), v, g);
         }
       }
     } else {

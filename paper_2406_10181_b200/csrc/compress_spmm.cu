@@ -56,7 +56,7 @@ struct Vec;
 template <>
 struct Vec<float> {
   static constexpr int CPL = 4;
-  __device__ __forceinline__ static void load(const float* p, float (&g)[4]) {
+  __device__ __forceinline__ static void load(const void* p, float (&g)[4]) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(p));
     g[0] = v.x, g[1] = v.y, g[2] = v.z, g[3] = v.w;
   }
@@ -64,7 +64,7 @@ struct Vec<float> {
 template <>
 struct Vec<bf16> {
   static constexpr int CPL = 8;
-  __device__ __forceinline__ static void load(const bf16* p, float (&g)[8]) {
+  __device__ __forceinline__ static void load(const void* p, float (&g)[8]) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
     const unsigned w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -125,32 +125,60 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
     const It t = item_at(item);
     const PMat& M = A.mat[t.mi];
     const int jl = t.j0 + lane * CPL;
-    const bool col_ok = jl < M.n;
-    const Tin* gcol = static_cast<const Tin*>(M.g) + jl;
+    // per-item constants in registers; a lane whose columns lie beyond n reads
+    // column 0 instead (valid memory) and its results are never written
+    const unsigned char* gcol = static_cast<const unsigned char*>(M.g) +
+                                (jl < M.n ? jl : 0) * static_cast<int>(sizeof(Tin));
+    const unsigned ldgb = static_cast<unsigned>(M.ldg * sizeof(Tin));  // < 4 GiB (host check)
     const EntryF* es = reinterpret_cast<const EntryF*>(ebuf + buf * A.ebuf_bytes) - t.elo;
-    if (A.pf_items && threadIdx.x == 32) {
-      // first touches of G from HBM, a few column tiles ahead: item (t', g)
-      // prefetches row slice g of tile t', so the r re-reads hit L2
-      const long long f = item + A.pf_items;
-      if (f < A.total) {
-        const It tf = item_at(f);
-        const PMat& F = A.mat[tf.mi];
-        tma_prefetch_2d(&F.tmap, tf.j0, (tf.b0 / kBG) * F.prow);
-      }
-    }
     float* z = zs + buf * kBG * LDS;
     mbar_wait(ebar + buf, (k >> 1) & 1);
 
-    // this warp's two bins as one entry stream [bin A | bin B], U loads in
-    // flight, the next batch issued before the current one is consumed
-    const int bA = t.b0 + warp, bB = t.b0 + warp + kSWarps;
-    const int eA0 = bA < A.d ? __ldg(M.ptr + bA) : 0, eA1 = bA < A.d ? __ldg(M.ptr + bA + 1) : 0;
-    const int eB0 = bB < A.d ? __ldg(M.ptr + bB) : 0, eB1 = bB < A.d ? __ldg(M.ptr + bB + 1) : 0;
-    const int nA = eA1 - eA0, T = nA + (eB1 - eB0);
-    float acc[CPL];
+    // this warp's bins: all U row gathers of a batch in flight at once, the
+    // full batches unpredicated (~7 instructions per entry), one predicated tail
+    for (int bb = warp; bb < kBG; bb += kSWarps) {
+      const int b = t.b0 + bb;
+      float acc[CPL];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
-    auto flush = [&](int bb) {
+      for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+      const int e0 = b < A.d ? __ldg(M.ptr + b) : 0, e1 = b < A.d ? __ldg(M.ptr + b + 1) : 0;
+      int e = e0;
+      for (; e + U <= e1; e += U) {
+        uint2 en[U];
+        float g[U][CPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const uint2*>(es + e + u);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float p = __uint_as_float(en[u].y);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p, g[u][c], acc[c]);
+        }
+      }
+      if (e < e1) {
+        const int cnt = e1 - e;
+        uint2 en[U];
+        float g[U][CPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (u < cnt) en[u] = *reinterpret_cast<const uint2*>(es + e + u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) g[u][c] = 0.0f;
+          if (u < cnt) Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (u < cnt) {
+            const float p = __uint_as_float(en[u].y);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p, g[u][c], acc[c]);
+          }
+      }
       // z[bb][lane*CPL + c], components rotated per lane group so that the
       // CPL stores of a warp each hit 32 distinct banks
       float* zr = z + bb * LDS + lane * CPL;
@@ -163,43 +191,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
           if (cc == q) v = acc[q];
         zr[cc] = v;
       }
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
-    };
-    float ga[U][CPL], gb[U][CPL], pa[U], pb[U];
-    auto load = [&](int t0, float (&g)[U][CPL], float (&p)[U]) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int tt = t0 + u;
-        p[u] = 0.0f;
-        if (tt < T) {
-          const uint2 en = *reinterpret_cast<const uint2*>(es + (tt < nA ? eA0 + tt : eB0 + tt - nA));
-          p[u] = __uint_as_float(en.y);
-          if (col_ok) Vec<Tin>::load(gcol + static_cast<long long>(static_cast<int>(en.x)) * M.ldg, g[u]);
-        }
-      }
-    };
-    auto consume = [&](int t0, const float (&g)[U][CPL], const float (&p)[U]) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int tt = t0 + u;
-        if (tt < T) {
-          if (tt == nA) flush(warp);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p[u], g[u][c], acc[c]);
-        }
-      }
-    };
-    if (T > 0) load(0, ga, pa);
-    for (int t0 = 0; t0 < T; t0 += 2 * U) {
-      if (t0 + U < T) load(t0 + U, gb, pb);
-      consume(t0, ga, pa);
-      if (t0 + U >= T) break;
-      if (t0 + 2 * U < T) load(t0 + 2 * U, ga, pa);
-      consume(t0 + U, gb, pb);
     }
-    if (T == nA) flush(warp);  // bin B empty (or both): bin A not flushed yet
-    flush(warp + kSWarps);
     __syncthreads();  // z[buf] complete; entry buffer `buf` free
     if (threadIdx.x == 0 && item + 2 * gridDim.x < A.total) stage(item + 2 * gridDim.x, buf);
     // Z^T[j0 + c][b0 + lane]: one 128-byte row segment per column
@@ -228,6 +220,7 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
     const Pair& pr = *J.pr;
     // 16-byte row segments: G aligned, columns and leading dimension in whole vectors
     if (reinterpret_cast<uintptr_t>(J.g) % 16 || pr.n % CPL || J.ldg % CPL) return false;
+    if (static_cast<unsigned long long>(pr.m) * J.ldg * sizeof(Tin) >= (1ull << 32)) return false;
     PMat& M = A.mat[i];
     M.g = J.g;
     M.ldg = J.ldg;
@@ -261,7 +254,7 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
   A.ebuf_bytes = round_up16(emax * 8 + 16);
   const int smem = 2 * kBG * (CT + 1) * static_cast<int>(sizeof(float)) + 2 * A.ebuf_bytes + 16;
   if (smem > 227 * 1024) return false;
-  auto kern = k_compress_spmm<Tin, 32 / CPL>;
+  auto kern = k_compress_spmm<Tin, 48 / CPL>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
   kern<<<grid, kSThreads, smem, st>>>(A);

@@ -47,15 +47,39 @@ __global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m
     c.y = 1.0 - pow(db2, static_cast<double>(t));
   }
   const T c1 = static_cast<T>(c.x), c2 = static_cast<T>(c.y);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x) {
-    const T gi = g[i];
-    const T mi = add_(mul_(b1, m[i]), mul_(omb1, gi));
-    const T vi = add_(mul_(b2, v[i]), mul_(mul_(omb2, gi), gi));
-    m[i] = mi;
-    v[i] = vi;
-    delta[i] = div_(div_(mi, c1), add_(sqrt_(div_(vi, c2)), eps));
+  auto one = [&](T gi, T& mo, T& vo) {  // returns delta; updates the moments in place
+    const T mi = add_(mul_(b1, mo), mul_(omb1, gi));
+    const T vi = add_(mul_(b2, vo), mul_(mul_(omb2, gi), gi));
+    mo = mi;
+    vo = vi;
+    return div_(div_(mi, c1), add_(sqrt_(div_(vi, c2)), eps));
+  };
+  long long i0 = 0;
+  if constexpr (sizeof(T) == 4) {
+    // 16-byte vector path (all of a layer's blocks are 16-byte aligned, cnt % 4 == 0)
+    if ((cnt & 3) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
+                            reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(delta)) & 15) == 0) {
+      const long long n4 = cnt >> 2;
+      for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+           i += (long long)gridDim.x * blockDim.x) {
+        const float4 gv = reinterpret_cast<const float4*>(g)[i];
+        float4 mv = reinterpret_cast<float4*>(m)[i];
+        float4 vv = reinterpret_cast<float4*>(v)[i];
+        float4 dv;
+        dv.x = one(gv.x, mv.x, vv.x);
+        dv.y = one(gv.y, mv.y, vv.y);
+        dv.z = one(gv.z, mv.z, vv.z);
+        dv.w = one(gv.w, mv.w, vv.w);
+        reinterpret_cast<float4*>(m)[i] = mv;
+        reinterpret_cast<float4*>(v)[i] = vv;
+        reinterpret_cast<float4*>(delta)[i] = dv;
+      }
+      i0 = cnt;
+    }
   }
+  for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    delta[i] = one(g[i], m[i], v[i]);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
