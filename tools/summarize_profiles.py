@@ -30,6 +30,8 @@ KEYS = [
     ("launch__block_size", "block"),
     ("launch__registers_per_thread", "regs/thread"),
     ("launch__shared_mem_per_block", "smem/block"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("smsp__average_warp_latency_issue_stalled_long_scoreboard", "stall long sb"),
 ]
 
 
@@ -59,8 +61,8 @@ def last_step(rows):
     # bench with --steps 1 --warmup 1: the step is the final run of launches
     # from the first stage-1 compress of the last step to the end.  Steps
     # start with a compress; find the last index where the layer-0 compress of
-    # a step begins (count of stage1 launches per step = n_layers).
-    idx = [i for i, r in enumerate(rows) if r[0].startswith("k_compress_stage1")]
+    # a step begins (count of stage-1 launches per step = n_layers).
+    idx = [i for i, r in enumerate(rows) if r[0].startswith("k_compress_")]
     if not idx:
         return rows
     per_step = len(idx) // 2 if len(idx) % 2 == 0 else len(idx)
@@ -113,7 +115,8 @@ def main():
                 f"{sum(n for n, _ in agg.values())} launches.\n")
     with open(f"profiles/{tag}_kernels.md", "w") as f:
         f.write(f"# {tag}: `ncu --set full` captures (one launch each, layer 8 of the step)\n\n")
-        for rep in ("prof_apply", "prof_stage1", "prof_stage2"):
+        reps = sorted(x[:-8] for x in os.listdir(src) if x.startswith("prof_") and x.endswith(".ncu-rep"))
+        for rep in reps:
             p = os.path.join(src, rep + ".ncu-rep")
             if not os.path.exists(p):
                 continue
