@@ -279,6 +279,67 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_c
   }
 }
 
+// Vector form (no shared memory): one warp = (matrix, band, 128-row block of
+// a, 8 of the band's columns).  Lane owns a = a0 + 4*lane .. +3 and reads
+// Delta^T[pos][a..a+3] with one 16-byte load (512 B per warp instruction, L2
+// hits: Delta^T is 4 MiB); per (column, entry) that is ONE memory instruction
+// for 4 outputs, against 1.5 shared-memory instructions per output in
+// k_build_y_smem (MIO-throttle bound).  Q entries are warp-uniform loads.
+constexpr int kYVJ = 8;  // band columns per warp task
+template <int BN, int KR>
+__global__ void __launch_bounds__(256) k_build_y_vec(const __grid_constant__ YArgs A) {
+  if (A.skip && *A.skip) return;
+  const int lane = threadIdx.x & 31;
+  const long long task = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (task >= A.total) return;
+  int mi = 0;
+  while (mi + 1 < A.count && task >= A.mat[mi].task_end) ++mi;
+  const YMat& M = A.mat[mi];
+  const long long lt = task - (mi ? A.mat[mi - 1].task_end : 0);
+  // task order: (band, column group, a-block), a-block fastest: the warps of
+  // one band share its Q entries in L1
+  const int ab = static_cast<int>(lt % A.ablocks);
+  const long long rest = lt / A.ablocks;
+  constexpr int NG = BN / kYVJ;
+  const int cg = static_cast<int>(rest % NG);
+  const int band = static_cast<int>(rest / NG);
+  const int d = A.d;
+  const int a = ab * 128 + 4 * lane;
+  const bool a_ok = a < d;  // d % 4 == 0 (host check)
+  float y[kYVJ][4];
+#pragma unroll
+  for (int t = 0; t < kYVJ; ++t) {
+    y[t][0] = y[t][1] = y[t][2] = y[t][3] = 0.0f;
+    const int j = band * BN + cg * kYVJ + t;
+    if (j < M.n) {
+#pragma unroll
+      for (int l = 0; l < KR; l += 4) {
+        const int4 pv = __ldg(reinterpret_cast<const int4*>(M.qpos + static_cast<long long>(j) * KR + l));
+        const float4 qv = __ldg(reinterpret_cast<const float4*>(M.qval + static_cast<long long>(j) * KR + l));
+        const int pp[4] = {pv.x, pv.y, pv.z, pv.w};
+        const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (a_ok) x = __ldg(reinterpret_cast<const float4*>(M.dT + static_cast<long long>(pp[e]) * d + a));
+          y[t][0] = fmaf(qq[e], x.x, y[t][0]);
+          y[t][1] = fmaf(qq[e], x.y, y[t][1]);
+          y[t][2] = fmaf(qq[e], x.z, y[t][2]);
+          y[t][3] = fmaf(qq[e], x.w, y[t][3]);
+        }
+      }
+    }
+  }
+  if (!a_ok) return;
+  float* base = M.yb + (static_cast<long long>(band) * d + a) * BN + cg * kYVJ;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {  // row a + c of the band block: kYVJ contiguous floats
+    float4* o = reinterpret_cast<float4*>(base + c * BN);
+#pragma unroll
+    for (int t = 0; t < kYVJ; t += 4) o[t / 4] = make_float4(y[t][c], y[t + 1][c], y[t + 2][c], y[t + 3][c]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // streaming apply
 // ---------------------------------------------------------------------------
@@ -521,6 +582,20 @@ void build_y_impl(const std::vector<DecJob>& jobs, const int* skip, cudaStream_t
   A.total = total;
   B.units = units;
   if (total == 0) return;
+  const char* vec_env = std::getenv("LSP_BUILD_Y_VEC");
+  if (p0.d % 4 == 0 && BN % kYVJ == 0 && !(vec_env && vec_env[0] == '0')) {
+    YArgs V = A;
+    V.ablocks = ceil_div(p0.d, 128);
+    long long tv = 0;
+    for (int i = 0; i < V.count; ++i) {
+      tv += static_cast<long long>(V.mat[i].nbands) * (BN / kYVJ) * V.ablocks;
+      V.mat[i].task_end = tv;
+    }
+    V.total = tv;
+    k_build_y_vec<BN, KR><<<static_cast<unsigned>((tv + 7) / 8), 256, 0, st>>>(V);
+    after_launch("build_y_vec");
+    return;
+  }
   if (use_smem) {
     const int smem = p0.d * 32 * static_cast<int>(sizeof(float)) + kYWarps * 2 * BN * KR * 4;
     auto kern = k_build_y_smem<BN, KR>;

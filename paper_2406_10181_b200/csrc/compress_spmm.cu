@@ -265,19 +265,24 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
 }  // namespace
 
 // Gather-form stage 1 (fp32 accumulation, fp32/bf16 G); false when the group
-// is not eligible or LSP_COMPRESS_SPMM is not 1.
+// is not eligible.  Chosen over the fixed-slot kernel where it measured faster
+// on B200: bf16 G (half the L2 traffic per column) and small groups (<= 256 MB
+// of G per launch: the slot kernel's per-CTA prologue dominates there, the
+// gather kernel is persistent).  LSP_COMPRESS_SPMM=1 / 0 forces it on / off.
 bool launch_compress_spmm_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, cudaStream_t st) {
   if (jobs.empty()) return false;
-  // opt-in (LSP_COMPRESS_SPMM=1) until it beats the fixed-slot kernel
-  const char* env = std::getenv("LSP_COMPRESS_SPMM");
-  if (!env || env[0] != '1') return false;
   const char* gen = std::getenv("LSP_COMPRESS_GENERIC");
   if (gen && gen[0] == '1') return false;
   const Pair& p0 = *jobs[0].pr;
-  if (p0.compute != LSP_F32) return false;
-  if (gdt == LSP_F32) return spmm_impl<float>(jobs, st);
-  if (gdt == LSP_BF16) return spmm_impl<bf16>(jobs, st);
-  return false;
+  if (p0.compute != LSP_F32 || (gdt != LSP_F32 && gdt != LSP_BF16)) return false;
+  const char* env = std::getenv("LSP_COMPRESS_SPMM");
+  if (env && env[0] == '0') return false;
+  if (!(env && env[0] == '1')) {
+    double gbytes = 0.0;
+    for (const S1Job& J : jobs) gbytes += static_cast<double>(J.pr->m) * J.pr->n * dtype_size(gdt);
+    if (gdt != LSP_BF16 && gbytes > 256.0 * (1 << 20)) return false;
+  }
+  return gdt == LSP_F32 ? spmm_impl<float>(jobs, st) : spmm_impl<bf16>(jobs, st);
 }
 
 }  // namespace lspb
