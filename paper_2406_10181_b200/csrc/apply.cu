@@ -551,7 +551,8 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
 }
 
 template <int BN, int KR>
-void build_y_impl(const std::vector<DecJob>& jobs, const int* skip, cudaStream_t st) {
+void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStream_t st) {
+  const std::vector<DecJob>& jobs = jobs_in;
   const Pair& p0 = *jobs[0].pr;
   const char* env = std::getenv("LSP_BUILD_Y_GLOBAL");
   const bool use_smem = p0.d <= kDsMaxD && !(env && env[0] == '1');

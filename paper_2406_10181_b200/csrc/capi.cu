@@ -177,6 +177,37 @@ const EntryF* Projector::csc_entries() {
   return csc_ent.as<EntryF>();
 }
 
+const Projector::PadTable& Projector::csc_padded() {
+  require(compute == LSP_F32, "csc_padded: fp32 projectors only");
+  if (!csc_pad) {
+    auto t = std::make_unique<PadTable>();
+    t->h_ptr.assign(d + 1, 0);
+    std::vector<EntryF> e;
+    std::vector<int32_t> perm;
+    for (int b = 0; b < d; ++b) {
+      const int k0 = h_csc_ptr[b], k1 = h_csc_ptr[b + 1];
+      for (int k = k0; k < k1; ++k) {
+        e.push_back(EntryF{h_csc_rows[k], static_cast<float>(h_val[h_csc_perm[k]])});
+        perm.push_back(h_csc_perm[k]);
+      }
+      const int cnt = k1 - k0, padded = (cnt + kPadU - 1) / kPadU * kPadU;
+      for (int k = cnt; k < padded; ++k) {
+        e.push_back(EntryF{h_csc_rows[k1 - 1], 0.0f});
+        perm.push_back(-1);
+      }
+      t->h_ptr[b + 1] = static_cast<int32_t>(e.size());
+    }
+    t->count = static_cast<long long>(e.size());
+    upload(t->ptr, t->h_ptr.data(), t->h_ptr.size() * sizeof(int32_t));
+    upload(t->ent, e.data(), e.size() * sizeof(EntryF));
+    upload(t->perm, perm.data(), perm.size() * sizeof(int32_t));
+    csc_pad = std::move(t);
+    launch_refresh_values(*this, nullptr);  // current device values
+    LSP_CUDA(cudaDeviceSynchronize());
+  }
+  return *csc_pad;
+}
+
 int* Pair::flag_ptr() {
   if (!flag.p) {
     flag.ensure(sizeof(int));

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
     while (mi + 1 < A.count && item >= A.mat[mi].item_end) ++mi;
     const long long lt = item - (mi ? A.mat[mi - 1].item_end : 0);
     const int b0 = static_cast<int>(lt % A.ngroups) * kBG;
-    const int elo = __ldg(A.mat[mi].ptr + b0) & ~1;  // 16-byte aligned start
+    const int elo = __ldg(A.mat[mi].ptr + b0);  // padded table: 64-byte aligned
     return It{mi, static_cast<int>(lt / A.ngroups) * CT, b0, elo};
   };
   // bulk-copy the CSC entries of an item's 32 bins into entry buffer `b`
@@ -134,51 +134,18 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
     float* z = zs + buf * kBG * LDS;
     mbar_wait(ebar + buf, (k >> 1) & 1);
 
-    // this warp's bins: all U row gathers of a batch in flight at once, the
-    // full batches unpredicated (~7 instructions per entry), one predicated tail
-    for (int bb = warp; bb < kBG; bb += kSWarps) {
-      const int b = t.b0 + bb;
-      float acc[CPL];
+    // This warp's two bins as one stream of U-entry batches (bins are padded
+    // to whole batches: pads repeat the bin's last row with value 0, an L1
+    // hit that adds +0), double-buffered: batch i+1's gathers are in flight
+    // while batch i is consumed; ~7 instructions per entry, no predicates.
+    const int bA = t.b0 + warp, bB = t.b0 + warp + kSWarps;
+    const int eA0 = bA < A.d ? __ldg(M.ptr + bA) : 0, eA1 = bA < A.d ? __ldg(M.ptr + bA + 1) : 0;
+    const int eB0 = bB < A.d ? __ldg(M.ptr + bB) : 0, eB1 = bB < A.d ? __ldg(M.ptr + bB + 1) : 0;
+    const int nA = (eA1 - eA0) / U, nb = nA + (eB1 - eB0) / U;
+    float acc[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
-      const int e0 = b < A.d ? __ldg(M.ptr + b) : 0, e1 = b < A.d ? __ldg(M.ptr + b + 1) : 0;
-      int e = e0;
-      for (; e + U <= e1; e += U) {
-        uint2 en[U];
-        float g[U][CPL];
-#pragma unroll
-        for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const uint2*>(es + e + u);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const float p = __uint_as_float(en[u].y);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p, g[u][c], acc[c]);
-        }
-      }
-      if (e < e1) {
-        const int cnt = e1 - e;
-        uint2 en[U];
-        float g[U][CPL];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (u < cnt) en[u] = *reinterpret_cast<const uint2*>(es + e + u);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) g[u][c] = 0.0f;
-          if (u < cnt) Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (u < cnt) {
-            const float p = __uint_as_float(en[u].y);
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p, g[u][c], acc[c]);
-          }
-      }
+    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    auto flush = [&](int bb) {
       // z[bb][lane*CPL + c], components rotated per lane group so that the
       // CPL stores of a warp each hit 32 distinct banks
       float* zr = z + bb * LDS + lane * CPL;
@@ -191,7 +158,45 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
           if (cc == q) v = acc[q];
         zr[cc] = v;
       }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    };
+    uint2 ena[U], enb[U];
+    float ga[U][CPL], gb[U][CPL];
+    auto load = [&](int i, uint2 (&en)[U], float (&g)[U][CPL]) {
+      const EntryF* src = es + (i < nA ? eA0 + i * U : eB0 + (i - nA) * U);
+#pragma unroll
+      for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const uint2*>(src + u);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
+    };
+    auto consume = [&](int i, const uint2 (&en)[U], const float (&g)[U][CPL]) {
+      if (i == nA) flush(warp);  // first batch of bin B: bin A complete
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float p = __uint_as_float(en[u].y);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p, g[u][c], acc[c]);
+      }
+    };
+    if constexpr (U * CPL <= 32) {  // registers for two batches: double-buffered
+      if (nb > 0) load(0, ena, ga);
+      for (int i = 0; i < nb; i += 2) {
+        if (i + 1 < nb) load(i + 1, enb, gb);
+        consume(i, ena, ga);
+        if (i + 1 >= nb) break;
+        if (i + 2 < nb) load(i + 2, ena, ga);
+        consume(i + 1, enb, gb);
+      }
+    } else {  // one (wider) batch in flight
+      for (int i = 0; i < nb; ++i) {
+        load(i, ena, ga);
+        consume(i, ena, ga);
+      }
     }
+    if (nA == nb) flush(warp);  // bin B empty: bin A not flushed in the loop
+    flush(warp + kSWarps);
     __syncthreads();  // z[buf] complete; entry buffer `buf` free
     if (threadIdx.x == 0 && item + 2 * gridDim.x < A.total) stage(item + 2 * gridDim.x, buf);
     // Z^T[j0 + c][b0 + lane]: one 128-byte row segment per column
@@ -224,8 +229,9 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
     PMat& M = A.mat[i];
     M.g = J.g;
     M.ldg = J.ldg;
-    M.ptr = pr.p->csc_ptr.as<int>();
-    M.ent = pr.p->csc_entries();
+    const Projector::PadTable& pt = pr.p->csc_padded();
+    M.ptr = pt.ptr.as<int>();
+    M.ent = pt.ent.as<EntryF>();
     M.zt = static_cast<float*>(J.zt);
     M.ldz = pr.ldz();
     M.n = pr.n;
@@ -247,14 +253,14 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
   // entry buffer: the largest 32-bin CSC range of any matrix (+16 B alignment slack)
   int emax = 0;
   for (const S1Job& J : jobs) {
-    const std::vector<int32_t>& ptr = J.pr->p->h_csc_ptr;
+    const std::vector<int32_t>& ptr = J.pr->p->csc_padded().h_ptr;
     for (int b0 = 0; b0 < p0.d; b0 += kBG)
-      emax = std::max(emax, ptr[std::min(b0 + kBG, p0.d)] - (ptr[b0] & ~1));
+      emax = std::max(emax, ptr[std::min(b0 + kBG, p0.d)] - ptr[b0]);
   }
   A.ebuf_bytes = round_up16(emax * 8 + 16);
   const int smem = 2 * kBG * (CT + 1) * static_cast<int>(sizeof(float)) + 2 * A.ebuf_bytes + 16;
   if (smem > 227 * 1024) return false;
-  auto kern = k_compress_spmm<Tin, 48 / CPL>;
+  auto kern = k_compress_spmm<Tin, Projector::kPadU>;  // U = pad unit
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
   kern<<<grid, kSThreads, smem, st>>>(A);

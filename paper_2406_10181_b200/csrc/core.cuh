@@ -110,6 +110,16 @@ struct Projector {
   // and kept current by refresh_values.
   const EntryF* csc_entries();
   DevBuf csc_ent;
+  // CSC entries with every bin padded to a multiple of kPadU entries (pads:
+  // the bin's last row, value 0, perm -1) for the gather-form compress.
+  static constexpr int kPadU = 8;
+  struct PadTable {
+    DevBuf ptr, ent, perm;
+    long long count = 0;
+    std::vector<int32_t> h_ptr;
+  };
+  std::unique_ptr<PadTable> csc_pad;
+  const PadTable& csc_padded();
   std::vector<std::pair<int, std::unique_ptr<DevBuf>>> scaled;
   // Re-derive CSC and chunk-table values from the CSR values on the device.
   void refresh_values(cudaStream_t st);
