@@ -29,7 +29,7 @@ namespace lspb {
 
 namespace {
 
-constexpr int kBG = 32;      // bins per item
+constexpr int kBG = 32;      // bins per item (kBG / kSWarps per warp; 64 measured slower)
 constexpr int kSWarps = 16;  // warps per CTA
 constexpr int kSThreads = kSWarps * 32;
 
@@ -138,10 +138,18 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
     // to whole batches: pads repeat the bin's last row with value 0, an L1
     // hit that adds +0), double-buffered: batch i+1's gathers are in flight
     // while batch i is consumed; ~7 instructions per entry, no predicates.
-    const int bA = t.b0 + warp, bB = t.b0 + warp + kSWarps;
-    const int eA0 = bA < A.d ? __ldg(M.ptr + bA) : 0, eA1 = bA < A.d ? __ldg(M.ptr + bA + 1) : 0;
-    const int eB0 = bB < A.d ? __ldg(M.ptr + bB) : 0, eB1 = bB < A.d ? __ldg(M.ptr + bB + 1) : 0;
-    const int nA = (eA1 - eA0) / U, nb = nA + (eB1 - eB0) / U;
+    constexpr int NBW = kBG / kSWarps;  // bins per warp: t.b0 + warp + w*kSWarps
+    int estart[NBW], bend[NBW + 1];     // entry start, cumulative batch counts
+    bend[0] = 0;
+#pragma unroll
+    for (int w = 0; w < NBW; ++w) {
+      const int b = t.b0 + warp + w * kSWarps;
+      const int e0 = b < A.d ? __ldg(M.ptr + b) : 0, e1 = b < A.d ? __ldg(M.ptr + b + 1) : 0;
+      estart[w] = e0;
+      bend[w + 1] = bend[w] + (e1 - e0) / U;
+    }
+    const int nb = bend[NBW];
+    int cur = 0;  // bin of the stream position being consumed
     float acc[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
@@ -164,7 +172,11 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
     uint2 ena[U], enb[U];
     float ga[U][CPL], gb[U][CPL];
     auto load = [&](int i, uint2 (&en)[U], float (&g)[U][CPL]) {
-      const EntryF* src = es + (i < nA ? eA0 + i * U : eB0 + (i - nA) * U);
+      int w = 0;
+#pragma unroll
+      for (int x = 1; x < NBW; ++x)
+        if (i >= bend[x]) w = x;
+      const EntryF* src = es + estart[w] + (i - bend[w]) * U;
 #pragma unroll
       for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const uint2*>(src + u);
 #pragma unroll
@@ -172,7 +184,10 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
         Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
     };
     auto consume = [&](int i, const uint2 (&en)[U], const float (&g)[U][CPL]) {
-      if (i == nA) flush(warp);  // first batch of bin B: bin A complete
+      while (cur < NBW - 1 && i >= bend[cur + 1]) {  // bins before position i complete
+        flush(warp + cur * kSWarps);
+        ++cur;
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float p = __uint_as_float(en[u].y);
@@ -195,16 +210,17 @@ __global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_con
         consume(i, ena, ga);
       }
     }
-    if (nA == nb) flush(warp);  // bin B empty: bin A not flushed in the loop
-    flush(warp + kSWarps);
+    for (; cur < NBW; ++cur) flush(warp + cur * kSWarps);  // the remaining bins
     __syncthreads();  // z[buf] complete; entry buffer `buf` free
     if (threadIdx.x == 0 && item + 2 * gridDim.x < A.total) stage(item + 2 * gridDim.x, buf);
-    // Z^T[j0 + c][b0 + lane]: one 128-byte row segment per column
-    const bool bin_ok = t.b0 + lane < A.d;
+    // Z^T[j0 + c][b0 + h*32 + lane]: 128-byte row segments per column
     for (int c = warp; c < CT; c += kSWarps) {
       const int j = t.j0 + c;
-      if (j < M.n && bin_ok)
-        M.zt[static_cast<long long>(j) * M.ldz + t.b0 + lane] = z[lane * LDS + c];
+      if (j >= M.n) continue;
+#pragma unroll
+      for (int h = 0; h < kBG / 32; ++h)
+        if (t.b0 + h * 32 + lane < A.d)
+          M.zt[static_cast<long long>(j) * M.ldz + t.b0 + h * 32 + lane] = z[(h * 32 + lane) * LDS + c];
     }
     // z[buf] is rewritten two items later, after the next __syncthreads
   }
