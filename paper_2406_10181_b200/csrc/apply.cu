@@ -725,28 +725,58 @@ bool run_bn(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha, double 
 
 // Fast path of launch_decompress_group for fp32 accumulation, W in fp32 or
 // bf16, r in {4, 8}; false (nothing enqueued) when not eligible.
-bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
+// Per-matrix eligibility of the Y path (column orientation).
+static bool y_eligible(const DecJob& J, lsp_dtype dt, double beta) {
+  const Pair& pr = *J.pr;
+  if (pr.compute != LSP_F32 || (dt != LSP_F32 && dt != LSP_BF16)) return false;
+  const int r = pr.p->r;
+  if ((r != 4 && r != 8) || pr.q->r != r) return false;
+  if (pr.d * 8 * 4 > kYMaxBytes) return false;
+  if (static_cast<long long>(pr.m) * J.ldo >= (1LL << 31)) return false;  // 32-bit offsets
+  if (beta != 0.0) {
+    const size_t es = dtype_size(dt);
+    if (J.in == nullptr || reinterpret_cast<uintptr_t>(J.in) % 16 || (J.ldi * es) % 16) return false;
+  }
+  const char* band = std::getenv("LSP_DECOMPRESS_BAND");
+  return !(band && band[0] == '1');
+}
+
+bool decompress_fast_eligible(const DecJob& J, lsp_dtype dt, double beta) {
+  return apply_x_eligible(J, dt, beta) || y_eligible(J, dt, beta);
+}
+
+bool launch_decompress_group_y(const std::vector<DecJob>& all_jobs, lsp_dtype dt, double alpha,
                                double beta, const int* skip_flag, cudaStream_t st, int phase) {
-  if (jobs.empty() || jobs.size() > static_cast<size_t>(kMaxGroup)) return false;
-  const Pair& p0 = *jobs[0].pr;
-  if (p0.compute != LSP_F32 || (dt != LSP_F32 && dt != LSP_BF16)) return false;
-  const int r = p0.p->r;
-  if (r != 4 && r != 8) return false;
-  for (const DecJob& J : jobs)
-    if (J.pr->q->r != r || J.pr->p->r != r) return false;
-  const int d = p0.d;
-  auto pick = [&](auto bn) -> bool {
-    constexpr int BN = decltype(bn)::value;
-    return r == 4 ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st, phase)
-                  : run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st, phase);
-  };
-  const char* bn_env = std::getenv("LSP_APPLY_BN");
-  const int bn_max = bn_env ? std::atoi(bn_env) : 32;
-  if (bn_max >= 32 && d * 32 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 32>{});
-  if (bn_max >= 16 && d * 16 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 16>{});
-  if (d * 16 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 16>{});
-  if (d * 8 * 4 <= kYMaxBytes) return pick(std::integral_constant<int, 8>{});
-  return false;
+  if (all_jobs.empty() || all_jobs.size() > static_cast<size_t>(kMaxGroup)) return false;
+  for (const DecJob& J : all_jobs)
+    if (!decompress_fast_eligible(J, dt, beta)) return false;
+  // n > m matrices go to the row orientation (apply_x.cu), the rest here;
+  // every matrix's path depends only on the matrix, never on its group
+  std::vector<DecJob> jobs, xjobs;
+  for (const DecJob& J : all_jobs) (apply_x_eligible(J, dt, beta) ? xjobs : jobs).push_back(J);
+  if (!jobs.empty()) {
+    const Pair& p0 = *jobs[0].pr;
+    const int r = p0.p->r, d = p0.d;
+    for (const DecJob& J : jobs)
+      require(J.pr->p->r == r && J.pr->d == d, "decompress group: matrices must share d and r");
+    auto pick = [&](auto bn) -> bool {
+      constexpr int BN = decltype(bn)::value;
+      return r == 4 ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st, phase)
+                    : run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st, phase);
+    };
+    const char* bn_env = std::getenv("LSP_APPLY_BN");
+    const int bn_max = bn_env ? std::atoi(bn_env) : 32;
+    bool ok = false;
+    if (bn_max >= 32 && d * 32 * 4 <= kYMaxBytes)
+      ok = pick(std::integral_constant<int, 32>{});
+    else if (d * 16 * 4 <= kYMaxBytes)
+      ok = pick(std::integral_constant<int, 16>{});
+    else
+      ok = pick(std::integral_constant<int, 8>{});
+    require(ok, "decompress: Y path rejected an eligible group");
+  }
+  if (!xjobs.empty()) launch_apply_x(xjobs, alpha, beta, skip_flag, st, phase);
+  return true;
 }
 
 }  // namespace lspb

@@ -138,6 +138,11 @@ struct Pair {
   DevBuf flag;  // int
   mutable DevBuf yb;  // float [nbands][d][BN]: Y = delta Q^T, band-blocked (apply.cu)
   void yb_ensure(size_t bytes) const { yb.ensure(bytes); }
+  mutable DevBuf xs, drow;  // X = P delta (row-swizzled) and delta row-major (apply_x.cu)
+  void xs_ensure(size_t xbytes, size_t dbytes) const {
+    xs.ensure(xbytes);
+    drow.ensure(dbytes);
+  }
   int ldz() const { return static_cast<int>(round_up(d, 4)); }
   int* flag_ptr();
 };
@@ -207,6 +212,12 @@ bool launch_decompress_group_tma(const std::vector<DecJob>& jobs, lsp_dtype dt, 
 // both kernels, only the Y build, or only the apply (after a Y build of the
 // same group on the same stream).
 constexpr int kPhaseBuild = 1, kPhaseApply = 2, kPhaseBoth = 3;
+// Does this matrix go through launch_decompress_group_y (row or column form)?
+bool decompress_fast_eligible(const DecJob& J, lsp_dtype dt, double beta);
+// Row-orientation apply (apply_x.cu) for n > m matrices.
+bool apply_x_eligible(const DecJob& J, lsp_dtype dt, double beta);
+void launch_apply_x(const std::vector<DecJob>& jobs, double alpha, double beta,
+                    const int* skip_flag, cudaStream_t st, int phase);
 bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                                double beta, const int* skip_flag, cudaStream_t st,
                                int phase = kPhaseBoth);

@@ -362,11 +362,18 @@ void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, doub
   for (const DecJob& J : jobs)
     require(J.pr->d == p0.d && J.pr->p->r == p0.p->r && J.pr->compute == p0.compute,
             "decompress group: matrices must share d, r and compute dtype");
-  if (!partials && !force_generic() && !force_band() &&
-      launch_decompress_group_y(jobs, dt, alpha, beta, skip_flag, st))
-    return;
+  std::vector<DecJob> rest;
+  if (!partials && !force_generic()) {
+    // fast paths per matrix (Y precompute / row orientation); the others below
+    std::vector<DecJob> fast;
+    for (const DecJob& J : jobs)
+      (decompress_fast_eligible(J, dt, beta) ? fast : rest).push_back(J);
+    if (!fast.empty()) launch_decompress_group_y(fast, dt, alpha, beta, skip_flag, st);
+    if (rest.empty()) return;
+  }
+  const std::vector<DecJob>& jobs_left = rest.empty() ? jobs : rest;
   if (!partials && !force_generic() &&
-      launch_decompress_group_tma(jobs, dt, alpha, beta, skip_flag, st))
+      launch_decompress_group_tma(jobs_left, dt, alpha, beta, skip_flag, st))
     return;
   LSP_DISPATCH_ACC(p0.compute, Tacc, {
     LSP_DISPATCH_STORAGE(dt, Tw, {
@@ -375,11 +382,11 @@ void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, doub
       auto run = [&](auto bn) {
         constexpr int BN = decltype(bn)::value;
         if (partials) {
-          decompress_impl<Tw, Tacc, BN, 0, true>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+          decompress_impl<Tw, Tacc, BN, 0, true>(jobs_left, alpha, beta, skip_flag, partials, nparts, st);
         } else if (r == 4) {
-          decompress_impl<Tw, Tacc, BN, 4, false>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+          decompress_impl<Tw, Tacc, BN, 4, false>(jobs_left, alpha, beta, skip_flag, partials, nparts, st);
         } else {
-          decompress_impl<Tw, Tacc, BN, 0, false>(jobs, alpha, beta, skip_flag, partials, nparts, st);
+          decompress_impl<Tw, Tacc, BN, 0, false>(jobs_left, alpha, beta, skip_flag, partials, nparts, st);
         }
       };
       if (Layout<Tw, Tacc, 32>{d, r}.total() <= kBudget)

@@ -30,7 +30,7 @@
 namespace lspb {
 
 bool encode_tmap_2d(CUtensorMap* map, const void* base, lsp_dtype dt, long long rows,
-                    long long cols, long long ld_elems, int box_cols, int box_rows) {
+                    long long cols, long long ld_elems, int box_cols, int box_rows, bool swz128) {
   static PFN_cuTensorMapEncodeTiled encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -51,7 +51,8 @@ bool encode_tmap_2d(CUtensorMap* map, const void* base, lsp_dtype dt, long long 
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   const CUresult rc = encode(map, t, 2, const_cast<void*>(base), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return rc == CUDA_SUCCESS;
@@ -61,26 +62,27 @@ namespace {
 struct MapKey {
   const void* p;
   long long rows, cols, ld;
-  int dt, bc, br;
+  int dt, bc, br, swz;
   bool operator<(const MapKey& o) const {
-    return std::tie(p, rows, cols, ld, dt, bc, br) < std::tie(o.p, o.rows, o.cols, o.ld, o.dt, o.bc, o.br);
+    return std::tie(p, rows, cols, ld, dt, bc, br, swz) <
+           std::tie(o.p, o.rows, o.cols, o.ld, o.dt, o.bc, o.br, o.swz);
   }
 };
 
 }  // namespace
 
 bool cached_tmap(CUtensorMap* out, const void* base, lsp_dtype dt, long long rows, long long cols,
-                 long long ld, int bc, int br) {
+                 long long ld, int bc, int br, bool swz128) {
   static std::mutex mu;
   static std::map<MapKey, CUtensorMap> cache;
-  const MapKey k{base, rows, cols, ld, static_cast<int>(dt), bc, br};
+  const MapKey k{base, rows, cols, ld, static_cast<int>(dt), bc, br, swz128 ? 1 : 0};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(k);
   if (it != cache.end()) {
     *out = it->second;
     return true;
   }
-  if (!encode_tmap_2d(out, base, dt, rows, cols, ld, bc, br)) return false;
+  if (!encode_tmap_2d(out, base, dt, rows, cols, ld, bc, br, swz128)) return false;
   if (cache.size() > 4096) cache.clear();
   cache.emplace(k, *out);
   return true;

@@ -99,23 +99,39 @@ std::vector<DecJob> apply_jobs(lsp_layer_s& L) {
   return jobs;
 }
 
+// The fast-path matrices of the layer (Y precompute / row orientation).
+std::vector<DecJob> fast_jobs(lsp_layer_s& L, std::vector<DecJob>* rest) {
+  std::vector<DecJob> fast;
+  const char* gen = std::getenv("LSP_DECOMPRESS_GENERIC");
+  const bool generic = gen && gen[0] == '1';
+  for (const DecJob& J : apply_jobs(L))
+    (!generic && decompress_fast_eligible(J, L.binds[0].wdt, 1.0) ? fast : *rest).push_back(J);
+  return fast;
+}
+
 void layer_apply_prepare(lsp_layer_s& L, cudaStream_t st) {
   check_bound(L);
-  L.prepared = !std::getenv("LSP_DECOMPRESS_GENERIC") && !std::getenv("LSP_DECOMPRESS_BAND") &&
-               launch_decompress_group_y(apply_jobs(L), L.binds[0].wdt, -1.0, 1.0,
-                                         L.adam.flag.as<int>(), st, kPhaseBuild);
+  std::vector<DecJob> rest;
+  const std::vector<DecJob> fast = fast_jobs(L, &rest);
+  L.prepared = !fast.empty() && launch_decompress_group_y(fast, L.binds[0].wdt, -1.0, 1.0,
+                                                          L.adam.flag.as<int>(), st, kPhaseBuild);
 }
 
 void layer_apply_finish(lsp_layer_s& L, double lr, cudaStream_t st) {
   check_bound(L);
-  if (L.prepared) {
-    L.prepared = false;
-    require(launch_decompress_group_y(apply_jobs(L), L.binds[0].wdt, -lr, 1.0,
-                                      L.adam.flag.as<int>(), st, kPhaseApply),
-            "layer_apply_finish: apply rejected after the Y build");
+  if (!L.prepared) {
+    layer_apply(L, lr, st);
     return;
   }
-  layer_apply(L, lr, st);
+  L.prepared = false;
+  std::vector<DecJob> rest;
+  const std::vector<DecJob> fast = fast_jobs(L, &rest);
+  require(launch_decompress_group_y(fast, L.binds[0].wdt, -lr, 1.0, L.adam.flag.as<int>(), st,
+                                    kPhaseApply),
+          "layer_apply_finish: apply rejected after the Y build");
+  if (!rest.empty())
+    launch_decompress_group(rest, L.binds[0].wdt, -lr, 1.0, L.adam.flag.as<int>(), nullptr,
+                            nullptr, st);
 }
 
 void layer_update(lsp_layer_s& L, double lr, bool check, cudaStream_t st) {

@@ -11,10 +11,11 @@ namespace lspb {
 // box of box_cols x box_rows elements.  Returns false if the driver refuses
 // (alignment etc.), so callers can fall back to cp.async.
 bool encode_tmap_2d(CUtensorMap* map, const void* base, lsp_dtype dt, long long rows,
-                    long long cols, long long ld_elems, int box_cols, int box_rows);
+                    long long cols, long long ld_elems, int box_cols, int box_rows,
+                    bool swz128 = false);
 // encode_tmap_2d behind a process-wide cache keyed on every argument.
 bool cached_tmap(CUtensorMap* out, const void* base, lsp_dtype dt, long long rows, long long cols,
-                 long long ld, int bc, int br);
+                 long long ld, int bc, int br, bool swz128 = false);
 
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -64,6 +65,22 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, i
                    reinterpret_cast<unsigned long long>(map)),
                "r"(x), "r"(y)
                : "memory");
+}
+
+// 2-D tensor tile shared -> global (bulk-group completion), and the group ops.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(smem_addr(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // Contiguous global -> shared bulk copy (size multiple of 16, 16-B aligned).

@@ -322,13 +322,14 @@ def test_launch_count_increases(cuda, port):
     assert lsp.launch_count() >= before + 2
 
 
-@pytest.mark.parametrize("path", ["y", "band", "generic"])
+@pytest.mark.parametrize("path", ["y", "rows", "band", "generic"])
 def test_decompress_paths_agree(cuda, port, path, monkeypatch):
     """The Y-precompute streaming kernel (apply.cu), the in-kernel Y_band TMA kernel
     and the generic cp.async kernel match the oracle (incl. ragged m, n, d not a
     multiple of 64, r = 8, wide d -> narrower bands, and the group tile split)."""
     monkeypatch.setenv("LSP_DECOMPRESS_GENERIC", "1" if path == "generic" else "0")
     monkeypatch.setenv("LSP_DECOMPRESS_BAND", "1" if path == "band" else "0")
+    monkeypatch.setenv("LSP_APPLY_ROWS", "1" if path == "rows" else "0")
     for (m, n, d, r) in [(777, 1000, 64, 4), (130, 4100, 128, 4), (4096, 96, 256, 4),
                          (300, 517, 100, 4), (513, 700, 96, 8), (200, 300, 2048, 4),
                          (100, 90, 4096, 4)]:
@@ -345,7 +346,9 @@ def test_decompress_paths_agree(cuda, port, path, monkeypatch):
 
 def test_decompress_y_bitwise_vs_band(cuda, port, monkeypatch):
     """Same arithmetic and summation order: the Y-precompute path is bitwise equal
-    to the in-kernel Y_band kernel, for fp32 and bf16 W."""
+    to the in-kernel Y_band kernel, for fp32 and bf16 W (column orientation
+    forced: the row orientation associates (P delta) Q^T and differs in rounding)."""
+    monkeypatch.setenv("LSP_APPLY_ROWS", "0")
     m, n, d = 1000, 1500, 256
     P, Q, pair = make(port, m, n, d, 4, 7)
     delta = dev(f32normal(d, (d, d)))
@@ -359,6 +362,26 @@ def test_decompress_y_bitwise_vs_band(cuda, port, monkeypatch):
             outs.append(w)
         torch.cuda.synchronize()
         assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("rows", ["1", "0"])
+def test_decompress_row_orientation(cuda, port, rows, monkeypatch):  # opt-in path and default
+    """The row-orientation apply (apply_x.cu, n > m, fp32): ragged m (not a multiple
+    of the 32-row band) and n (not a multiple of the 128-column tile), r = 4 and 8,
+    in-place apply and decompress-only output, against the oracle; and against
+    the column orientation within fp32 rounding."""
+    monkeypatch.setenv("LSP_APPLY_ROWS", rows)
+    for (m, n, d, r) in [(77, 1000, 64, 4), (130, 4100, 128, 4), (513, 700, 96, 8),
+                         (1000, 4096, 1024, 4), (32, 129, 32, 4)]:
+        P, Q, pair = make(port, m, n, d, r, m + 3 * n)
+        delta = f32normal(d + 1, (d, d))
+        w0 = f32normal(n + 1, (m, n), 0.02)
+        w = dev(w0)
+        pair.decompress_apply(dev(delta), 1e-3, w)
+        ref = port.decompress_apply(P, Q, delta, 1e-3, w0)
+        assert rel(host(w) - w0, ref - w0) < 1e-5, (m, n, d, r)
+        out = host(pair.decompress(dev(delta)))
+        assert rel(out, port.decompress(P, Q, delta)) < 1e-5, (m, n, d, r)
 
 
 def _skewed(m, d, r, seed, hot):

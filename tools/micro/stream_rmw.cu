@@ -123,6 +123,70 @@ __global__ void ring(const __grid_constant__ RArgs A) {
     }
 }
 
+
+// ring2: tiles of NB boxes side by side (box = 32 fp32 cols x TR rows, 128B
+// swizzle), i.e. a TR x 32*NB tile whose rows are 128*NB bytes of W; lane =
+// row reads 16-byte chunks (swizzle makes the 8-lane phases conflict-free),
+// results written back in place and TMA-stored (the row-orientation apply).
+struct R2Args { CUtensorMap map; float* w; int m, n, nb, tr, stages, ng, nc, reserve, tile_bytes; };
+__global__ void ring2(const __grid_constant__ R2Args A) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* rg = sm + A.reserve;
+  unsigned long long* full = (unsigned long long*)(rg + A.stages * A.tile_bytes);
+  unsigned long long* empty = full + A.stages;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, S = A.stages;
+  const int per_group = A.nc / A.ng;
+  if (tid == 0) { for (int s = 0; s < S; ++s) { mb_init(full + s, 1); mb_init(empty + s, 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  __syncthreads();
+  const int tc = 32 * A.nb;
+  const int ntc = (A.n + tc - 1) / tc, nrb = (A.m + A.tr - 1) / A.tr;
+  const long long tiles = (long long)ntc * nrb;
+  if (warp == A.nc) {
+    if (lane == 0) {
+      unsigned long long pol; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int s = 0;
+      for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++s) {
+        const int rb = t / ntc, cb = t % ntc;  // concurrent tiles: same rows, adjacent columns
+        const int st = s % S;
+        if (s >= S) mb_wait(empty + st, ((s / S) - 1) & 1);
+        mb_expect(full + st, A.tile_bytes);
+        for (int b = 0; b < A.nb; ++b)
+          asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+            ::"r"(sa(rg + st * A.tile_bytes + b * 32 * 4 * A.tr)), "l"(&A.map), "r"(cb * tc + b * 32), "r"(rb * A.tr), "r"(sa(full + st)), "l"(pol) : "memory");
+      }
+    }
+    return;
+  }
+  const int g = warp / per_group, wg = warp % per_group;
+  int s = 0;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++s) {
+    if (s % A.ng != g) continue;
+    const int rb = t / ntc, cb = t % ntc;
+    const int st = s % S;
+    mb_wait(full + st, (s / S) & 1);
+    unsigned char* tile = rg + st * A.tile_bytes;
+    // rows: lane + 32*k; column chunks (16 B): spread over the group's warps
+    for (int rr = lane; rr < A.tr; rr += 32)
+      for (int ch = wg; ch < 8 * A.nb; ch += per_group) {
+        const int b = ch / 8, c = ch % 8;
+        float4* p = (float4*)(tile + b * 32 * 4 * A.tr + rr * 128 + ((c ^ (rr & 7)) * 16));
+        float4 v = *p;
+        v.x = 0.999f * v.x + 1e-3f; v.y = 0.999f * v.y + 1e-3f; v.z = 0.999f * v.z + 1e-3f; v.w = 0.999f * v.w + 1e-3f;
+        *p = v;
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(per_group * 32) : "memory");
+    if (wg == 0 && lane == 0) {
+      for (int b = 0; b < A.nb; ++b)
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&A.map), "r"(cb * tc + b * 32), "r"(rb * A.tr), "r"(sa(tile + b * 32 * 4 * A.tr)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mb_arrive(empty + st);
+    }
+  }
+}
+
 int main() {
   CK(cudaSetDevice(0)); int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int m = 4096 * 7, n = 11008;  // ~1.26 GB fp32
@@ -135,6 +199,22 @@ int main() {
       printf("band_plain bn=%d blocks/SM=%d: %.0f GB/s\n", bn, bpsm, timeit([&] { band_plain<<<sms * bpsm, 256>>>(w, m, n, bn); }));
   void* fn = nullptr; cudaDriverEntryPointQueryResult q; CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
   auto enc = (PFN_cuTensorMapEncodeTiled)fn;
+  struct C2 { int nb, tr, stages, ng, nc, reserve; } c2s[] = {
+    {4, 32, 4, 2, 16, 128 * 1024}, {4, 32, 5, 2, 16, 128 * 1024}, {4, 32, 4, 4, 16, 128 * 1024},
+    {8, 32, 2, 2, 16, 128 * 1024}, {4, 64, 2, 2, 16, 128 * 1024}, {2, 32, 8, 2, 16, 128 * 1024},
+    {4, 32, 8, 2, 16, 0}, {8, 32, 6, 2, 16, 0}};
+  for (auto c : c2s) {
+    R2Args A{}; A.w = w; A.m = m; A.n = n; A.nb = c.nb; A.tr = c.tr; A.stages = c.stages; A.ng = c.ng; A.nc = c.nc; A.reserve = c.reserve;
+    A.tile_bytes = c.nb * 32 * 4 * c.tr;
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m}; cuuint64_t str[1] = {(cuuint64_t)n * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)c.tr}; cuuint32_t es[2] = {1, 1};
+    if (enc(&A.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode2 failed\n"); continue; }
+    int smem = c.reserve + c.stages * A.tile_bytes + 2 * c.stages * 8 + 1024;
+    if (smem > 227 * 1024) { printf("skip smem %d\n", smem); continue; }
+    CK(cudaFuncSetAttribute(ring2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    double gbs = timeit([&] { ring2<<<sms, (c.nc + 1) * 32, smem>>>(A); });
+    printf("ring2 rows=%3d B x %d, tr=%d S=%d ng=%d reserve=%3dK: %.0f GB/s\n", 128 * c.nb, 1, c.tr, c.stages, c.ng, c.reserve / 1024, gbs);
+  }
   struct Cfg { int bn, tr, stages, ng, nc, reserve, ts; } cfgs[] = {
     {32, 64, 8, 1, 16, 128 * 1024, 0}, {32, 64, 8, 4, 16, 128 * 1024, 0}, {32, 64, 8, 8, 16, 128 * 1024, 0},
     {32, 64, 8, 4, 16, 128 * 1024, 1}, {32, 64, 8, 8, 16, 128 * 1024, 1},
