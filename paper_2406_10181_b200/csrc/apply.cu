@@ -45,6 +45,51 @@ constexpr int kMaxStages = 16;
 constexpr int kYChunk = 16 * 1024;      // bulk-copy granule for the Y block
 constexpr int kTileElems = 4096;        // W elements per ring tile (BN x TR)
 
+
+// A projector row's (or column's) KR entries, read with the widest vectors KR
+// allows (KR in {2, 4, 8}); order is the reference's l = 0 .. KR-1.
+template <int KR>
+struct Ent {
+  int p[KR];
+  float v[KR];
+};
+template <int KR>
+__device__ __forceinline__ Ent<KR> ent_ldg(const int* pp, const float* vp) {
+  Ent<KR> e;
+  if constexpr (KR == 2) {
+    const int2 a = __ldg(reinterpret_cast<const int2*>(pp));
+    const float2 b = __ldg(reinterpret_cast<const float2*>(vp));
+    e.p[0] = a.x, e.p[1] = a.y, e.v[0] = b.x, e.v[1] = b.y;
+  } else {
+#pragma unroll
+    for (int l = 0; l < KR; l += 4) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(pp + l));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(vp + l));
+      e.p[l] = a.x, e.p[l + 1] = a.y, e.p[l + 2] = a.z, e.p[l + 3] = a.w;
+      e.v[l] = b.x, e.v[l + 1] = b.y, e.v[l + 2] = b.z, e.v[l + 3] = b.w;
+    }
+  }
+  return e;
+}
+template <int KR>
+__device__ __forceinline__ Ent<KR> ent_gen(const int* pp, const float* vp) {  // shared via generic
+  Ent<KR> e;
+  if constexpr (KR == 2) {
+    const int2 a = *reinterpret_cast<const int2*>(pp);
+    const float2 b = *reinterpret_cast<const float2*>(vp);
+    e.p[0] = a.x, e.p[1] = a.y, e.v[0] = b.x, e.v[1] = b.y;
+  } else {
+#pragma unroll
+    for (int l = 0; l < KR; l += 4) {
+      const int4 a = *reinterpret_cast<const int4*>(pp + l);
+      const float4 b = *reinterpret_cast<const float4*>(vp + l);
+      e.p[l] = a.x, e.p[l + 1] = a.y, e.p[l + 2] = a.z, e.p[l + 3] = a.w;
+      e.v[l] = b.x, e.v[l + 1] = b.y, e.v[l + 2] = b.z, e.v[l + 3] = b.w;
+    }
+  }
+  return e;
+}
+
 // ---------------------------------------------------------------------------
 // Y build
 // ---------------------------------------------------------------------------
@@ -88,23 +133,10 @@ __global__ void __launch_bounds__(256) k_build_y(const __grid_constant__ YArgs A
     y1[jj] = 0.0f;
     const int j = band * BN + jj;
     if (j < M.n) {
-      int p[KR];
-      float q[KR];
-      if constexpr (KR % 4 == 0) {
-#pragma unroll
-        for (int l = 0; l < KR; l += 4) {
-          const int4 pv = __ldg(reinterpret_cast<const int4*>(M.qpos + static_cast<long long>(j) * KR + l));
-          const float4 qv = __ldg(reinterpret_cast<const float4*>(M.qval + static_cast<long long>(j) * KR + l));
-          p[l] = pv.x, p[l + 1] = pv.y, p[l + 2] = pv.z, p[l + 3] = pv.w;
-          q[l] = qv.x, q[l + 1] = qv.y, q[l + 2] = qv.z, q[l + 3] = qv.w;
-        }
-      } else {
-#pragma unroll
-        for (int l = 0; l < KR; ++l) {
-          p[l] = __ldg(M.qpos + static_cast<long long>(j) * KR + l);
-          q[l] = __ldg(M.qval + static_cast<long long>(j) * KR + l);
-        }
-      }
+      const Ent<KR> en = ent_ldg<KR>(M.qpos + static_cast<long long>(j) * KR,
+                                     M.qval + static_cast<long long>(j) * KR);
+      const int* p = en.p;
+      const float* q = en.v;
 #pragma unroll
       for (int l = 0; l < KR; ++l) {
         const float* row = M.dT + static_cast<long long>(p[l]) * d;
@@ -259,15 +291,9 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_c
         // columns beyond n have zero entries (fetch), so y stays 0: no branch,
         // the BN column chains interleave freely
         y[jj] = 0.0f;
+        const Ent<KR> en = ent_gen<KR>(sp + jj * KR, sv + jj * KR);
 #pragma unroll
-        for (int l = 0; l < KR; l += 4) {
-          const int4 pv = *reinterpret_cast<const int4*>(sp + jj * KR + l);
-          const float4 qv = *reinterpret_cast<const float4*>(sv + jj * KR + l);
-          y[jj] = fmaf(qv.x, ds[pv.x * 32 + lane], y[jj]);
-          y[jj] = fmaf(qv.y, ds[pv.y * 32 + lane], y[jj]);
-          y[jj] = fmaf(qv.z, ds[pv.z * 32 + lane], y[jj]);
-          y[jj] = fmaf(qv.w, ds[pv.w * 32 + lane], y[jj]);
-        }
+        for (int l = 0; l < KR; ++l) y[jj] = fmaf(en.v[l], ds[en.p[l] * 32 + lane], y[jj]);
       }
       if (a < d) {
         float4* o = reinterpret_cast<float4*>(M.yb + (static_cast<long long>(band) * d + a) * BN);
@@ -312,21 +338,16 @@ __global__ void __launch_bounds__(256) k_build_y_vec(const __grid_constant__ YAr
     y[t][0] = y[t][1] = y[t][2] = y[t][3] = 0.0f;
     const int j = band * BN + cg * kYVJ + t;
     if (j < M.n) {
+      const Ent<KR> en = ent_ldg<KR>(M.qpos + static_cast<long long>(j) * KR,
+                                     M.qval + static_cast<long long>(j) * KR);
 #pragma unroll
-      for (int l = 0; l < KR; l += 4) {
-        const int4 pv = __ldg(reinterpret_cast<const int4*>(M.qpos + static_cast<long long>(j) * KR + l));
-        const float4 qv = __ldg(reinterpret_cast<const float4*>(M.qval + static_cast<long long>(j) * KR + l));
-        const int pp[4] = {pv.x, pv.y, pv.z, pv.w};
-        const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (a_ok) x = __ldg(reinterpret_cast<const float4*>(M.dT + static_cast<long long>(pp[e]) * d + a));
-          y[t][0] = fmaf(qq[e], x.x, y[t][0]);
-          y[t][1] = fmaf(qq[e], x.y, y[t][1]);
-          y[t][2] = fmaf(qq[e], x.z, y[t][2]);
-          y[t][3] = fmaf(qq[e], x.w, y[t][3]);
-        }
+      for (int e = 0; e < KR; ++e) {
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a_ok) x = __ldg(reinterpret_cast<const float4*>(M.dT + static_cast<long long>(en.p[e]) * d + a));
+        y[t][0] = fmaf(en.v[e], x.x, y[t][0]);
+        y[t][1] = fmaf(en.v[e], x.y, y[t][1]);
+        y[t][2] = fmaf(en.v[e], x.z, y[t][2]);
+        y[t][3] = fmaf(en.v[e], x.w, y[t][3]);
       }
     }
   }
@@ -382,6 +403,16 @@ __device__ __forceinline__ Unit unit_at(const AArgs& A, long long u) {
 __device__ __forceinline__ float lds_f32(unsigned addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int2 lds_v2i(unsigned addr) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 lds_v2f(unsigned addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ int4 lds_v4i(unsigned addr) {
@@ -457,7 +488,9 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
           const int r0 = rb * TR;
           const int nrows = min(TR, M.m - r0);
           unsigned char* base = ring + st * A.stage_bytes;
-          const unsigned eb = static_cast<unsigned>(nrows) * KR * 4u;
+          // odd row counts with KR = 2: round up to the 16-byte bulk-copy
+          // granule (the projector arrays carry 16 bytes of slack)
+          const unsigned eb = (static_cast<unsigned>(nrows) * KR * 4u + 15u) & ~15u;
           mbar_arrive_expect_tx(full + st, (USE_IN ? A.w_bytes : 0) + 2u * eb);
           if (USE_IN) tma_load_2d(base, &M.tmap, U.band * BN, r0, full + st, pol);
           bulk_load(base + A.w_bytes, M.ppos_scaled + static_cast<long long>(r0) * KR, eb,
@@ -517,16 +550,24 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
       const unsigned vq = base + A.w_bytes + A.e_bytes + q0 * KR * 4u;
       constexpr int kq = WPG * RPW;  // row step between a lane's rows
       auto row = [&](int v) {
-        float acc = 0.0f;
+        int pp[KR];
+        float vv[KR];
+        if constexpr (KR == 2) {
+          const int2 a = lds_v2i(pq + v * kq * KR * 4u);
+          const float2 b = lds_v2f(vq + v * kq * KR * 4u);
+          pp[0] = a.x, pp[1] = a.y, vv[0] = b.x, vv[1] = b.y;
+        } else {
 #pragma unroll
-        for (int l = 0; l < KR; l += 4) {
-          const int4 pp = lds_v4i(pq + (v * kq * KR + l) * 4u);
-          const float4 vv = lds_v4f(vq + (v * kq * KR + l) * 4u);
-          acc = l == 0 ? vv.x * lds_f32(y_lane + pp.x) : fmaf(vv.x, lds_f32(y_lane + pp.x), acc);
-          acc = fmaf(vv.y, lds_f32(y_lane + pp.y), acc);
-          acc = fmaf(vv.z, lds_f32(y_lane + pp.z), acc);
-          acc = fmaf(vv.w, lds_f32(y_lane + pp.w), acc);
+          for (int l = 0; l < KR; l += 4) {
+            const int4 a = lds_v4i(pq + (v * kq * KR + l) * 4u);
+            const float4 b = lds_v4f(vq + (v * kq * KR + l) * 4u);
+            pp[l] = a.x, pp[l + 1] = a.y, pp[l + 2] = a.z, pp[l + 3] = a.w;
+            vv[l] = b.x, vv[l + 1] = b.y, vv[l + 2] = b.z, vv[l + 3] = b.w;
+          }
         }
+        float acc = vv[0] * lds_f32(y_lane + pp[0]);
+#pragma unroll
+        for (int l = 1; l < KR; ++l) acc = fmaf(vv[l], lds_f32(y_lane + pp[l]), acc);
         float res = alpha * acc;
         if (USE_IN) res = fmaf(beta, lds_w<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw))), res);
         return cvt<Tw>(res);
@@ -730,7 +771,7 @@ static bool y_eligible(const DecJob& J, lsp_dtype dt, double beta) {
   const Pair& pr = *J.pr;
   if (pr.compute != LSP_F32 || (dt != LSP_F32 && dt != LSP_BF16)) return false;
   const int r = pr.p->r;
-  if ((r != 4 && r != 8) || pr.q->r != r) return false;
+  if ((r != 2 && r != 4 && r != 8) || pr.q->r != r) return false;
   if (pr.d * 8 * 4 > kYMaxBytes) return false;
   if (static_cast<long long>(pr.m) * J.ldo >= (1LL << 31)) return false;  // 32-bit offsets
   if (beta != 0.0) {
@@ -761,8 +802,9 @@ bool launch_decompress_group_y(const std::vector<DecJob>& all_jobs, lsp_dtype dt
       require(J.pr->p->r == r && J.pr->d == d, "decompress group: matrices must share d and r");
     auto pick = [&](auto bn) -> bool {
       constexpr int BN = decltype(bn)::value;
-      return r == 4 ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st, phase)
-                    : run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st, phase);
+      return r == 4   ? run_bn<BN, 4>(jobs, dt, alpha, beta, skip_flag, st, phase)
+             : r == 8 ? run_bn<BN, 8>(jobs, dt, alpha, beta, skip_flag, st, phase)
+                      : run_bn<BN, 2>(jobs, dt, alpha, beta, skip_flag, st, phase);
     };
     const char* bn_env = std::getenv("LSP_APPLY_BN");
     const int bn_max = bn_env ? std::atoi(bn_env) : 32;

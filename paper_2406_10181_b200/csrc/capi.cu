@@ -64,7 +64,7 @@ int guard(F&& f) {
 
 // ---- Projector ---------------------------------------------------------------
 static void upload(DevBuf& b, const void* src, size_t bytes) {
-  b.ensure(std::max<size_t>(bytes, 16));
+  b.ensure(bytes + 16);  // 16 bytes of slack: 16-byte bulk copies may round up past the end
   if (bytes) LSP_CUDA(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
 }
 

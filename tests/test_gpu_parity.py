@@ -332,7 +332,7 @@ def test_decompress_paths_agree(cuda, port, path, monkeypatch):
     monkeypatch.setenv("LSP_APPLY_ROWS", "1" if path == "rows" else "0")
     for (m, n, d, r) in [(777, 1000, 64, 4), (130, 4100, 128, 4), (4096, 96, 256, 4),
                          (300, 517, 100, 4), (513, 700, 96, 8), (200, 300, 2048, 4),
-                         (100, 90, 4096, 4)]:
+                         (100, 90, 4096, 4), (515, 700, 96, 2), (129, 333, 4096, 2)]:
         P, Q, pair = make(port, m, n, d, r, m + n)
         delta = f32normal(d, (d, d))
         w0 = f32normal(n, (m, n), 0.02)

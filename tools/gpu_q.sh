@@ -1,7 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x -k "decompress or layer" 2>&1 | tail -2
-b() { timeout 600 python bench.py --config $1 --steps 3 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/b.json 2>gpurun_out/b.err; python -c "
-import json;d=json.load(open('gpurun_out/b.json'));b=d['breakdown'];print('$1 $2', 'ms/step',round(d['ms_per_step'],2),{k:round(v,2) for k,v in b.items() if k.endswith('ms_per_step')})" || tail -3 gpurun_out/b.err; }
-b c4 rows; b c2 rows; LSP_APPLY_ROWS=0 b c2 cols
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum
-ncu --metrics $M --clock-control none -k regex:"k_apply_x" -s 2 -c 1 --csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/n.csv 2>/dev/null; python tools/ncu_csv.py gpurun_out/n.csv | sed 's/bytes_//g'
+timeout 900 python tools/dbg_r2.py "515,700,96,2;3,64,32,2"
+timeout 1500 python -m pytest tests -q -m gpu --timeout 240 2>&1 | tail -3
