@@ -12,8 +12,14 @@ if ROOT not in sys.path:
 GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 
 
+@pytest.hookimpl(tryfirst=True)  # before pytest-timeout reads its settings
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and liblsp_b200.so")
+    # a kernel that deadlocks (e.g. an mbarrier expecting bytes that never
+    # arrive) must fail its test, not hang the whole run: per-test time limit
+    # via pytest-timeout when no --timeout was given on the command line
+    if config.pluginmanager.hasplugin("timeout") and not config.getoption("timeout", None):
+        config.option.timeout = 600
 
 
 @pytest.fixture(scope="session")
