@@ -291,6 +291,31 @@ int lsp_projector_gram(lsp_projector_t a, lsp_projector_t b, double* out,
 int lsp_reproject_state(lsp_adam_t st, lsp_pair_t old_pair, lsp_pair_t new_pair,
                         lsp_transfer_kind kind, lsp_stream_t stream);
 
+/* ----------------------------------------------------------------------------
+ * Bias-gated refresh: maybe_update (proj/src/trainer.cpp:74-112; result struct
+ * proj/include/lsp/trainer.hpp:95-104).  Keeps the pair when the relative bias
+ * on grad_sub is <= alpha; otherwise draws a fresh pair with init_sparse
+ * (seeds derive_seed(reinit_seed, 1 | 2)), fits it on grad_sub plus the
+ * non-zero extra targets (fit seed derive_seed(reinit_seed, 3)), and
+ * reprojects `st` IN PLACE into the new subspace.  On refresh the new
+ * projectors and pair are returned (caller-owned; the old ones are untouched),
+ * otherwise *new_p = *new_q = *new_pair = NULL.  A zero grad_sub skips the
+ * check (bias NaN).  SYNCHRONOUS.
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  int refreshed;
+  int fit_timed_out; /* fit report timed_out || stalled */
+  int skipped_zero_grad;
+  int fit_steps;
+  double bias_before;
+  double bias_after;
+} lsp_maybe_update_result;
+int lsp_maybe_update(lsp_pair_t pair, lsp_adam_t st, const void* grad_sub, int64_t ld,
+                     lsp_dtype dtype, const void* const* extra, int n_extra, int r,
+                     double alpha, const lsp_fit_config* fit_cfg, lsp_transfer_kind transfer,
+                     uint64_t reinit_seed, lsp_projector_t* new_p, lsp_projector_t* new_q,
+                     lsp_pair_t* new_pair, lsp_maybe_update_result* res, lsp_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,11 @@ class Oracle:
                                              C.c_char_p, C.c_int64]
             L.ref_time_step.argtypes = pair + [_f64p, _f64p, C.c_double, C.c_int, C.c_int,
                                                C.POINTER(C.c_double)]
+            L.ref_maybe_update.argtypes = pair + [_f64p, _f64p, C.c_int64, _f64p, C.c_int, _f64p,
+                                                  C.c_int, C.c_double, C.c_double, C.c_double,
+                                                  C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                  C.c_uint64,
+                                                  _i32p, _f64p, _i32p, _f64p, _f64p, _f64p, _f64p]
 
     # -- plumbing ---------------------------------------------------------
     def _fn(self, name):
@@ -230,6 +235,30 @@ class Oracle:
         buf = C.create_string_buffer(int(need))
         self.lib.ref_save_projector(P.n_rows, P.d, P.r, P.pos, P.val, buf, need)
         return buf.value.decode()
+
+    def maybe_update(self, P, Q, m, v, step, grad, extras, r, alpha, fit_alpha=0.1,
+                     reg_beta=0.0, step_size=1e-2, max_steps=500, timeout_steps=500,
+                     reg_kind=0, transfer=0, reinit_seed=0):
+        """Reference maybe_update (trainer.cpp:74-112).  Returns (newP, newQ, m, v,
+        result dict); newP/newQ equal P/Q when not refreshed."""
+        d = P.d
+        mm, nn = P.n_rows, Q.n_rows
+        npos, nval = np.zeros(mm * r, np.int32), np.zeros(mm * r)
+        qpos, qval = np.zeros(nn * r, np.int32), np.zeros(nn * r)
+        mo, vo = np.zeros((d, d)), np.zeros((d, d))
+        res = np.zeros(6)
+        ex = self._f64(np.stack(extras)) if extras else np.zeros(1)
+        self._check(self.lib.ref_maybe_update(
+            *self._pair_args(P, Q), self._f64(m), self._f64(v), step, self._f64(grad),
+            len(extras), ex, r, alpha, fit_alpha, reg_beta, step_size, max_steps, timeout_steps,
+            reg_kind,
+            transfer, reinit_seed, npos, nval, qpos, qval, mo, vo, res))
+        out = dict(refreshed=bool(res[0]), fit_timed_out=bool(res[1]),
+                   skipped_zero_grad=bool(res[2]), bias_before=res[3], bias_after=res[4],
+                   fit_steps=int(res[5]))
+        if not out["refreshed"]:
+            return P, Q, mo, vo, out
+        return (Projector(mm, d, r, npos, nval), Projector(nn, d, r, qpos, qval), mo, vo, out)
 
     def time_step(self, P, Q, g, w0, lr, count, threads) -> float:
         secs = C.c_double()

@@ -313,4 +313,47 @@ int ref_time_step(int m, int n, int d, int r, const int32_t* ppos, const double*
   });
 }
 
+// proj/src/trainer.cpp:74-112 (maybe_update), the reference's own code.
+// state = {m_in, v_in, step}; on refresh the new pair (r nonzeros per row) is
+// written to np_*/nq_* and the reprojected state to m_out/v_out (unchanged
+// copies otherwise).  result = {refreshed, fit_timed_out, skipped_zero_grad,
+// bias_before, bias_after, fit_steps}.
+int ref_maybe_update(int m, int n, int d, int r_old, const int32_t* ppos, const double* pval,
+                     const int32_t* qpos, const double* qval, const double* m_in,
+                     const double* v_in, int64_t step, const double* grad, int n_extra,
+                     const double* extra, int r, double alpha, double fit_alpha, double reg_beta,
+                     double step_size,
+                     int max_steps, int timeout_steps, int reg_kind, int transfer,
+                     uint64_t reinit_seed, int32_t* np_pos, double* np_val, int32_t* nq_pos,
+                     double* nq_val, double* m_out, double* v_out, double* result) {
+  return guard([&] {
+    auto pair = to_pair(m, n, d, r_old, ppos, pval, qpos, qval);
+    lsp::SubspaceOptState st = lsp::make_opt_state(d);
+    st.m = to_mat(d, d, m_in);
+    st.v = to_mat(d, d, v_in);
+    st.step = step;
+    lsp::TrainConfig cfg;
+    cfg.r = r;
+    cfg.alpha = alpha;
+    cfg.fit = to_fit_cfg(fit_alpha, reg_beta, step_size, max_steps, timeout_steps, reg_kind);
+    cfg.transfer = transfer ? lsp::TransferKind::kMatrixSquare : lsp::TransferKind::kEntrywiseSquare;
+    const auto out = lsp::maybe_update(to_mat(m, n, grad), pair, st, cfg,
+                                       to_targets(n_extra, m, n, extra), reinit_seed);
+    const int rr = out.pair.p.r;
+    std::copy(out.pair.p.positions.begin(), out.pair.p.positions.end(), np_pos);
+    std::copy(out.pair.p.values.begin(), out.pair.p.values.end(), np_val);
+    std::copy(out.pair.q.positions.begin(), out.pair.q.positions.end(), nq_pos);
+    std::copy(out.pair.q.values.begin(), out.pair.q.values.end(), nq_val);
+    (void)rr;
+    from_mat(out.state.m, m_out);
+    from_mat(out.state.v, v_out);
+    result[0] = out.refreshed ? 1.0 : 0.0;
+    result[1] = out.fit_timed_out ? 1.0 : 0.0;
+    result[2] = out.skipped_zero_grad ? 1.0 : 0.0;
+    result[3] = out.bias_before;
+    result[4] = out.bias_after;
+    result[5] = out.fit_steps;
+  });
+}
+
 }  // extern "C"

@@ -36,6 +36,7 @@ from .projector import (  # noqa: F401
     init_sparse,
     load_projector,
     projector_gram,
+    maybe_update,
     reproject_state,
     save_projector,
     step,
@@ -45,7 +46,7 @@ from .projector import (  # noqa: F401
 
 __all__ = [
     "AdamState", "DevicePair", "Layer", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
-    "identity_pattern", "init_sparse", "load_projector", "projector_gram", "reproject_state",
+    "identity_pattern", "init_sparse", "load_projector", "projector_gram", "reproject_state", "maybe_update",
     "save_projector", "step", "subsample_size", "update", "LspError", "InvalidArgument",
     "NumericError", "IoError", "CudaError", "Layout", "lib", "library_path", "launch_count",
 ]

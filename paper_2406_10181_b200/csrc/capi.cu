@@ -3,6 +3,7 @@
 // device kernels.  No compute happens on the host except index generation.
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <string>
 
@@ -711,6 +712,76 @@ int lsp_update(lsp_pair_t pair, lsp_adam_t a, const void* s_t, void* w, int64_t 
     check_ld(ldw, pair->n, "update");
     update_impl(*pair, *a, s_t, w, ldw, w_dtype, lr, as_stream(stream), true);
   });
+}
+
+}  // extern "C"
+
+// ---- bias-gated projector refresh (proj/src/trainer.cpp:74-112) -----------------
+extern "C" {
+
+int lsp_maybe_update(lsp_pair_t pair, lsp_adam_t st, const void* grad_sub, int64_t ld,
+                     lsp_dtype dtype, const void* const* extra, int n_extra, int r,
+                     double alpha, const lsp_fit_config* fit_cfg, lsp_transfer_kind transfer,
+                     uint64_t reinit_seed, lsp_projector_t* new_p, lsp_projector_t* new_q,
+                     lsp_pair_t* new_pair, lsp_maybe_update_result* res, lsp_stream_t stream) {
+  lsp_projector_t np = nullptr, nq = nullptr;
+  lsp_pair_t npair = nullptr;
+  const int rc = guard([&] {
+    require(pair && st && grad_sub && fit_cfg && new_p && new_q && new_pair && res,
+            "maybe_update: null argument");
+    require(n_extra >= 0 && (n_extra == 0 || extra), "maybe_update: bad extra targets");
+    check_ld(ld, pair->n, "maybe_update");
+    *new_p = nullptr, *new_q = nullptr, *new_pair = nullptr;
+    cudaStream_t s = as_stream(stream);
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    *res = lsp_maybe_update_result{0, 0, 0, 0, 0.0, 0.0};
+    // trainer.cpp:82-87: a zero gradient skips the check
+    if (sumsq_sync(*pair, pair->m, pair->n, grad_sub, ld, dtype, s) == 0.0) {
+      res->skipped_zero_grad = 1;
+      res->bias_before = res->bias_after = nan;
+      return;
+    }
+    auto call = [](int code) {
+      if (code != LSP_OK) fail(code, g_last_error);
+    };
+    call(lsp_relative_bias(pair, grad_sub, ld, dtype, &res->bias_before, stream));
+    res->bias_after = res->bias_before;
+    if (res->bias_before <= alpha) return;  // trainer.cpp:88
+    // trainer.cpp:90-93: fresh pair from the refresh seed
+    const lspb::Projector& op = *pair->p;
+    const lspb::Projector& oq = *pair->q;
+    std::vector<int32_t> pp(static_cast<size_t>(op.n_rows) * r), qp(static_cast<size_t>(oq.n_rows) * r);
+    std::vector<double> pv(pp.size()), qv(qp.size());
+    call(lsp_init_sparse(op.n_rows, op.d, r, lsp_derive_seed(reinit_seed, 1, 0), pp.data(), pv.data()));
+    call(lsp_init_sparse(oq.n_rows, oq.d, r, lsp_derive_seed(reinit_seed, 2, 0), qp.data(), qv.data()));
+    call(lsp_projector_create(op.n_rows, op.d, r, pp.data(), pv.data(), op.compute, &np));
+    call(lsp_projector_create(oq.n_rows, oq.d, r, qp.data(), qv.data(), oq.compute, &nq));
+    call(lsp_pair_create(np, nq, &npair));
+    // trainer.cpp:95-103: fit on grad_sub plus the non-zero extra targets
+    std::vector<const void*> targets{grad_sub};
+    for (int i = 0; i < n_extra; ++i) {
+      require(extra[i] != nullptr, "maybe_update: null extra target");
+      if (sumsq_sync(*pair, pair->m, pair->n, extra[i], ld, dtype, s) > 0.0) targets.push_back(extra[i]);
+    }
+    lsp_fit_config cfg = *fit_cfg;
+    cfg.seed = lsp_derive_seed(reinit_seed, 3, 0);
+    lsp_fit_report rep{};
+    call(lsp_fit(npair, targets.data(), static_cast<int>(targets.size()), ld, dtype, &cfg, &rep,
+                 nullptr, 0, stream));
+    // trainer.cpp:105-110: state transfer, report, bias on the new pair
+    call(lsp_reproject_state(st, pair, npair, transfer, stream));
+    res->refreshed = 1;
+    res->fit_timed_out = (rep.timed_out || rep.stalled) ? 1 : 0;
+    res->fit_steps = rep.steps;
+    call(lsp_relative_bias(npair, grad_sub, ld, dtype, &res->bias_after, stream));
+    *new_p = np, *new_q = nq, *new_pair = npair;
+  });
+  if (rc != LSP_OK) {  // nothing half-built escapes
+    if (npair) lsp_pair_destroy(npair);
+    if (np) lsp_projector_destroy(np);
+    if (nq) lsp_projector_destroy(nq);
+  }
+  return rc;
 }
 
 }  // extern "C"

@@ -158,6 +158,17 @@ class DeviceProjector:
         self._h = h
 
     @classmethod
+    def _adopt(cls, handle, compute):
+        """Wrap a projector handle created by the library (takes ownership)."""
+        obj = cls.__new__(cls)
+        n_rows, d, r = C.c_int(), C.c_int(), C.c_int()
+        lib.projector_shape(handle, C.byref(n_rows), C.byref(d), C.byref(r))
+        obj.n_rows, obj.d, obj.r = n_rows.value, d.value, r.value
+        obj.compute = compute
+        obj._h = handle
+        return obj
+
+    @classmethod
     def random(cls, n_rows: int, d: int, r: int, seed: int, compute="f32"):
         pos, val = init_sparse(n_rows, d, r, seed)
         return cls(n_rows, d, r, pos, val, compute)
@@ -220,9 +231,11 @@ class FitReport:
 class DevicePair:
     """ProjectorPair (projector.hpp:32-36) with its device workspace."""
 
-    def __init__(self, p: DeviceProjector, q: DeviceProjector):
-        h = C.c_void_p()
-        lib.pair_create(p.handle, q.handle, C.byref(h))
+    def __init__(self, p: DeviceProjector, q: DeviceProjector, handle=None):
+        h = handle
+        if h is None:
+            h = C.c_void_p()
+            lib.pair_create(p.handle, q.handle, C.byref(h))
         self._h, self.p, self.q = h, p, q
         self.m, self.n, self.d = p.n_rows, q.n_rows, p.d
         self.compute = p.compute
@@ -527,6 +540,38 @@ def projector_gram(a: DeviceProjector, b: DeviceProjector, stream=None):
     out = torch.empty(a.d, b.d, dtype=torch.float64, device="cuda")
     lib.projector_gram(a.handle, b.handle, C.c_void_p(out.data_ptr()), _stream(stream))
     return out
+
+
+class MaybeUpdateResultC(C.Structure):
+    _fields_ = [("refreshed", C.c_int), ("fit_timed_out", C.c_int),
+                ("skipped_zero_grad", C.c_int), ("fit_steps", C.c_int),
+                ("bias_before", C.c_double), ("bias_after", C.c_double)]
+
+
+def maybe_update(pair: DevicePair, adam: AdamState, grad_sub, extra_targets=(), r: int = 4,
+                 alpha: float = 0.5, fit: Optional[FitConfig] = None, transfer: int = 0,
+                 reinit_seed: int = 0, stream=None):
+    """Bias-gated projector refresh (trainer.cpp:74-112): returns (pair, result)
+    where pair is the SAME pair when the relative bias on grad_sub is within
+    alpha, else a new fitted DevicePair; adam is reprojected in place."""
+    targets = [grad_sub] + list(extra_targets)
+    arr, _, ld, dt = pair._targets(targets)
+    extra = (C.c_void_p * max(1, len(extra_targets)))(*arr[1:]) if extra_targets else None
+    c = (fit or FitConfig()).c()
+    np_h, nq_h, npair = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    res = MaybeUpdateResultC()
+    lib.maybe_update(pair.handle, adam.handle, C.c_void_p(arr[0]), ld, int(dt), extra,
+                     len(extra_targets), int(r), float(alpha), C.byref(c), int(transfer),
+                     C.c_uint64(reinit_seed), C.byref(np_h), C.byref(nq_h), C.byref(npair),
+                     C.byref(res), _stream(stream))
+    out = dict(refreshed=bool(res.refreshed), fit_timed_out=bool(res.fit_timed_out),
+               skipped_zero_grad=bool(res.skipped_zero_grad), fit_steps=res.fit_steps,
+               bias_before=res.bias_before, bias_after=res.bias_after)
+    if not res.refreshed:
+        return pair, out
+    p = DeviceProjector._adopt(np_h, pair.compute)
+    q = DeviceProjector._adopt(nq_h, pair.compute)
+    return DevicePair(p, q, handle=npair), out
 
 
 def reproject_state(adam: AdamState, old_pair: DevicePair, new_pair: DevicePair, kind: int = 0,

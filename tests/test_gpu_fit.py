@@ -179,3 +179,59 @@ def test_reproject_larger_vs_oracle(cuda, port):
         mo, vo, _ = a.get()
         mref, vref = port.reproject_state(oP, oQ, nP, nQ, mm, vv, kind)
         assert rel(mo, mref) < 1e-12 and rel(vo, vref) < 1e-12
+
+
+@pytest.mark.parametrize("transfer", [0, 1])
+def test_maybe_update_vs_reference(cuda, reference, transfer):
+    """Bias-gated refresh (trainer.cpp:74-112) against the reference's own
+    maybe_update: the gate decision, the fresh projectors (indices bit-exact),
+    the fit trajectory length and fitted values, the reprojected Adam moments
+    and the bias before/after.  fp64 device compute."""
+    m, n, d, r_old, r = 64, 48, 16, 4, 3
+    P = reference.init_sparse(m, d, r_old, 11)
+    Q = reference.init_sparse(n, d, r_old, 12)
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal((m, n))
+    extras = [rng.standard_normal((m, n)), np.zeros((m, n)), rng.standard_normal((m, n))]
+    mm, vv = rng.standard_normal((d, d)), rng.standard_normal((d, d)) ** 2
+    kw = dict(alpha=0.5, fit_alpha=0.1, step_size=1e-2, max_steps=40, timeout_steps=40,
+              transfer=transfer, reinit_seed=99)
+    nP, nQ, mref, vref, res_ref = reference.maybe_update(P, Q, mm, vv, 3, g, extras, r, **kw)
+    assert res_ref["refreshed"]
+
+    pair = dpair(P, Q)
+    adam = lsp.AdamState(d, compute="f64")
+    adam.set(mm, vv, 3)
+    fit = lsp.FitConfig(alpha=0.1, step_size=1e-2, max_steps=40, timeout_steps=40)
+    new_pair, res = lsp.maybe_update(pair, adam, dev(g), [dev(x) for x in extras], r=r,
+                                     alpha=0.5, fit=fit, transfer=transfer, reinit_seed=99)
+    assert res["refreshed"] and new_pair is not pair
+    assert res["fit_steps"] == res_ref["fit_steps"]
+    assert res["fit_timed_out"] == res_ref["fit_timed_out"]
+    assert abs(res["bias_before"] - res_ref["bias_before"]) < 1e-10 * res_ref["bias_before"]
+    assert abs(res["bias_after"] - res_ref["bias_after"]) < 1e-8 * res_ref["bias_after"]
+    pp, pv = new_pair.p.get()
+    qp, qv = new_pair.q.get()
+    assert np.array_equal(pp, nP.pos) and np.array_equal(qp, nQ.pos)
+    assert rel(pv, nP.val) < 1e-9 and rel(qv, nQ.val) < 1e-9
+    mo, vo, st = adam.get()
+    assert st == 3
+    assert rel(mo, mref) < 1e-9 and rel(vo, vref) < 1e-9
+
+
+def test_maybe_update_gate_and_zero_grad(cuda, reference):
+    """Bias within alpha: same pair, state untouched; zero gradient: skipped, NaN bias."""
+    m, n, d, r = 40, 30, 8, 2
+    P, Q = reference.init_sparse(m, d, r, 1), reference.init_sparse(n, d, r, 2)
+    g = np.random.default_rng(1).standard_normal((m, n))
+    mm, vv = np.ones((d, d)), np.ones((d, d))
+    _, _, _, _, res_ref = reference.maybe_update(P, Q, mm, vv, 1, g, [], r, alpha=1e9)
+    pair, adam = dpair(P, Q), lsp.AdamState(d, compute="f64")
+    adam.set(mm, vv, 1)
+    same, res = lsp.maybe_update(pair, adam, dev(g), [], r=r, alpha=1e9)
+    assert same is pair and not res["refreshed"] and not res_ref["refreshed"]
+    assert abs(res["bias_before"] - res_ref["bias_before"]) < 1e-10 * res_ref["bias_before"]
+    mo, vo, _ = adam.get()
+    assert np.array_equal(mo, mm) and np.array_equal(vo, vv)
+    same, res = lsp.maybe_update(pair, adam, dev(np.zeros((m, n))), [], r=r, alpha=0.1)
+    assert same is pair and res["skipped_zero_grad"] and np.isnan(res["bias_before"])
