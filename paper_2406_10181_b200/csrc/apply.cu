@@ -43,7 +43,7 @@ constexpr int kNG = 2;                  // consumer groups
 constexpr int kAThreads = (kNC + 2) * 32;
 constexpr int kMaxStages = 16;
 constexpr int kYChunk = 16 * 1024;      // bulk-copy granule for the Y block
-constexpr int kTileElems = 4096;        // W elements per ring tile (BN x TR)
+constexpr int kTileBytes = 16384;       // W bytes per ring tile (BN x TR elements)
 
 
 // A projector row's (or column's) KR entries, read with the widest vectors KR
@@ -442,7 +442,8 @@ __device__ __forceinline__ float lds_w(unsigned addr) {
 
 template <typename Tw, int BN, int KR, bool USE_IN>
 __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant__ AArgs A) {
-  constexpr int TR = kTileElems / BN < 256 ? kTileElems / BN : 256;  // W rows per tile
+  constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
+  constexpr int TR = TRW < 256 ? TRW : 256;  // W rows per tile (16 KB of W; <= 256 TMA box rows)
   constexpr int RPW = 32 / BN;         // rows per warp instruction
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (A.skip && *A.skip) return;
@@ -654,7 +655,8 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
 template <typename Tw, int BN, int KR>
 bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, const int* skip,
                 cudaStream_t st) {
-  constexpr int TR = kTileElems / BN < 256 ? kTileElems / BN : 256;
+  constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
+  constexpr int TR = TRW < 256 ? TRW : 256;
   const Pair& p0 = *jobs[0].pr;
   const bool use_in = beta != 0.0;
   AArgs A{};
