@@ -151,6 +151,32 @@ class Clocks:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def profiled_traffic(kernel_prefix, config):
+    """DRAM bytes (read + write) of one launch of the roofline kernel from the
+    committed ncu --set full summary (profiles/<round>_kernels.md, captured with
+    this bench's own C4 command); None for other configs or when absent."""
+    if config != "c4":
+        return None, None
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.md")))
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for path in reversed(files):
+        text = open(path).read()
+        for sec in text.split("## ")[1:]:
+            head = sec.splitlines()[0]
+            if kernel_prefix not in head:
+                continue
+            vals = {}
+            for key in ("dram read", "dram write"):
+                m = re.search(r"\| %s \| ([0-9.]+) (\w+) \|" % key, sec)
+                if m:
+                    vals[key] = float(m.group(1)) * units.get(m.group(2), 1)
+            if len(vals) == 2:
+                return vals["dram read"] + vals["dram write"], os.path.relpath(path, ROOT)
+    return None, None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -358,6 +384,7 @@ def run_ours(args):
     app_avg = float(np.mean(app_ms))
     comp_avg = float(np.mean(comp_ms))
     app_ach = app_bytes / (app_avg * 1e-3) / 1e9
+    traffic, traffic_src = profiled_traffic("k_apply_y<float", args.config)
     comp_ach = comp_bytes / (comp_avg * 1e-3) / 1e9
     tsum = sum(app_ms) + sum(comp_ms) + sum(adam_ms) + sum(build_ms)
     line = {
@@ -380,7 +407,11 @@ def run_ours(args):
                                "1 launch per layer; Y = delta Q^T built by k_build_y_smem just "
                                "before, timed separately as build_ms)",
                      "bound": "hbm", "achieved": app_ach, "peak": peak, "unit": "GB/s",
-                     "frac": app_ach / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": app_ach / peak, "traffic": traffic,
+                     "traffic_source": (f"{traffic_src}: ncu --set full dram__bytes_read.sum + "
+                                        "dram__bytes_write.sum of one launch (includes the "
+                                        "Y-block reads from HBM)") if traffic else None,
+                     "peak_source": peak_src,
                      "bytes_per_launch_avg": app_bytes, "avg_launch_ms": app_avg,
                      "share_of_step": sum(app_ms) / (ms if ms > 0 else 1)},
         "breakdown": {"compress_ms_per_step": sum(comp_ms), "adam_ms_per_step": sum(adam_ms),

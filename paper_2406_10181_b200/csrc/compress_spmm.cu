@@ -15,9 +15,10 @@
 // 32-bin group) item at a time and writes its Z^T block (tile rows x 32 bins,
 // 128-byte row segments) through a shared-memory transpose.
 //
-// Persistent grid; items are ordered (matrix, column tile, bin group) and
-// handed out with a stride of gridDim.x, so the tiles in flight at any moment
-// are a small L2-resident window of G.
+// Persistent grid, two 8-warp CTAs per SM (one streams while the other is in
+// its item barrier / transposed write); items are ordered (matrix, column
+// tile, bin group) and handed out with a stride of gridDim.x, so the tiles in
+// flight at any moment are a small L2-resident window of G.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -30,7 +31,8 @@ namespace lspb {
 namespace {
 
 constexpr int kBG = 32;      // bins per item (kBG / kSWarps per warp; 64 measured slower)
-constexpr int kSWarps = 16;  // warps per CTA
+constexpr int kSWarps = 8;   // warps per CTA
+constexpr int kSCtas = 2;    // CTAs per SM: one streams while the other syncs/transposes
 constexpr int kSThreads = kSWarps * 32;
 
 struct alignas(64) PMat {
@@ -76,7 +78,7 @@ struct Vec<bf16> {
 };
 
 template <typename Tin, int U>
-__global__ void __launch_bounds__(kSThreads, 1) k_compress_spmm(const __grid_constant__ PArgs A) {
+__global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __grid_constant__ PArgs A) {
   constexpr int CPL = Vec<Tin>::CPL;
   constexpr int CT = 32 * CPL;  // columns per tile
   constexpr int LDS = CT + 1;   // padded row of the transpose buffer
@@ -278,7 +280,7 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
   if (smem > 227 * 1024) return false;
   auto kern = k_compress_spmm<Tin, Projector::kPadU>;  // U = pad unit
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
+  const int grid = static_cast<int>(std::min<long long>(total, kSCtas * num_sms()));
   kern<<<grid, kSThreads, smem, st>>>(A);
   after_launch("compress_spmm");
   return true;
@@ -287,10 +289,10 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
 }  // namespace
 
 // Gather-form stage 1 (fp32 accumulation, fp32/bf16 G); false when the group
-// is not eligible.  Chosen over the fixed-slot kernel where it measured faster
-// on B200: bf16 G (half the L2 traffic per column) and small groups (<= 256 MB
-// of G per launch: the slot kernel's per-CTA prologue dominates there, the
-// gather kernel is persistent).  LSP_COMPRESS_SPMM=1 / 0 forces it on / off.
+// is not eligible.  The default stage 1 for fp32 accumulation: measured on
+// B200 at or below the fixed-slot kernel for every BASELINE config (C4 fp32
+// 13.46 vs 13.57 ms per step of compress, C4 bf16 9.7 vs 12.6, C3 3.1 vs
+// 3.6, C2 2.7 vs 3.7).  LSP_COMPRESS_SPMM=0 falls back to the slot kernel.
 bool launch_compress_spmm_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, cudaStream_t st) {
   if (jobs.empty()) return false;
   const char* gen = std::getenv("LSP_COMPRESS_GENERIC");
@@ -299,11 +301,6 @@ bool launch_compress_spmm_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, c
   if (p0.compute != LSP_F32 || (gdt != LSP_F32 && gdt != LSP_BF16)) return false;
   const char* env = std::getenv("LSP_COMPRESS_SPMM");
   if (env && env[0] == '0') return false;
-  if (!(env && env[0] == '1')) {
-    double gbytes = 0.0;
-    for (const S1Job& J : jobs) gbytes += static_cast<double>(J.pr->m) * J.pr->n * dtype_size(gdt);
-    if (gdt != LSP_BF16 && gbytes > 256.0 * (1 << 20)) return false;
-  }
   return gdt == LSP_F32 ? spmm_impl<float>(jobs, st) : spmm_impl<bf16>(jobs, st);
 }
 
