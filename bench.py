@@ -404,7 +404,7 @@ def run_ours(args):
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},
         "roofline": {"kernel": "k_apply_y (grouped streaming decompress-and-apply W -= lr P Y, "
-                               "1 launch per layer; Y = delta Q^T built by k_build_y_smem just "
+                               "1 launch per layer; Y = delta Q^T built by k_build_y_vec just "
                                "before, timed separately as build_ms)",
                      "bound": "hbm", "achieved": app_ach, "peak": peak, "unit": "GB/s",
                      "frac": app_ach / peak, "traffic": traffic,

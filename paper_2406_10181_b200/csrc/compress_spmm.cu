@@ -141,17 +141,25 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
     // hit that adds +0), double-buffered: batch i+1's gathers are in flight
     // while batch i is consumed; ~7 instructions per entry, no predicates.
     constexpr int NBW = kBG / kSWarps;  // bins per warp: t.b0 + warp + w*kSWarps
-    int estart[NBW], bend[NBW + 1];     // entry start, cumulative batch counts
-    bend[0] = 0;
+    // per-bin entry start and batch count, indexed only with compile-time
+    // indices (register-resident; dynamic lookups go through select chains)
+    int es_w[NBW], nb_w[NBW];
+    int nb = 0;
 #pragma unroll
     for (int w = 0; w < NBW; ++w) {
       const int b = t.b0 + warp + w * kSWarps;
       const int e0 = b < A.d ? __ldg(M.ptr + b) : 0, e1 = b < A.d ? __ldg(M.ptr + b + 1) : 0;
-      estart[w] = e0;
-      bend[w + 1] = bend[w] + (e1 - e0) / U;
+      es_w[w] = e0;
+      nb_w[w] = (e1 - e0) / U;
+      nb += nb_w[w];
     }
-    const int nb = bend[NBW];
-    int cur = 0;  // bin of the stream position being consumed
+    auto sel = [](const int (&arr)[NBW], int w) {
+      int r = arr[0];
+#pragma unroll
+      for (int x = 1; x < NBW; ++x)
+        if (w == x) r = arr[x];
+      return r;
+    };
     float acc[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
@@ -171,25 +179,38 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
     };
+    // load cursor (bin lb, next batch at lsrc, lleft batches left in the bin)
+    int lb = 0, lleft = nb_w[0];
+    const EntryF* lsrc = es + es_w[0];
+    auto load_skip = [&]() {
+      while (lleft == 0 && lb < NBW - 1) {
+        ++lb;
+        lleft = sel(nb_w, lb);
+        lsrc = es + sel(es_w, lb);
+      }
+    };
+    load_skip();
     uint2 ena[U], enb[U];
     float ga[U][CPL], gb[U][CPL];
-    auto load = [&](int i, uint2 (&en)[U], float (&g)[U][CPL]) {
-      int w = 0;
-#pragma unroll
-      for (int x = 1; x < NBW; ++x)
-        if (i >= bend[x]) w = x;
-      const EntryF* src = es + estart[w] + (i - bend[w]) * U;
+    auto load = [&](uint2 (&en)[U], float (&g)[U][CPL]) {
+      const EntryF* src = lsrc;
+      lsrc += U;
+      if (--lleft == 0) load_skip();
 #pragma unroll
       for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const uint2*>(src + u);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
     };
-    auto consume = [&](int i, const uint2 (&en)[U], const float (&g)[U][CPL]) {
-      while (cur < NBW - 1 && i >= bend[cur + 1]) {  // bins before position i complete
-        flush(warp + cur * kSWarps);
-        ++cur;
+    // consume cursor: bin cb, cleft batches left in it; completed bins flushed
+    int cb = 0, cleft = nb_w[0];
+    auto consume = [&](const uint2 (&en)[U], const float (&g)[U][CPL]) {
+      while (cleft == 0 && cb < NBW - 1) {
+        flush(warp + cb * kSWarps);
+        ++cb;
+        cleft = sel(nb_w, cb);
       }
+      --cleft;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float p = __uint_as_float(en[u].y);
@@ -198,21 +219,21 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
       }
     };
     if constexpr (U * CPL <= 32) {  // registers for two batches: double-buffered
-      if (nb > 0) load(0, ena, ga);
+      if (nb > 0) load(ena, ga);
       for (int i = 0; i < nb; i += 2) {
-        if (i + 1 < nb) load(i + 1, enb, gb);
-        consume(i, ena, ga);
+        if (i + 1 < nb) load(enb, gb);
+        consume(ena, ga);
         if (i + 1 >= nb) break;
-        if (i + 2 < nb) load(i + 2, ena, ga);
-        consume(i + 1, enb, gb);
+        if (i + 2 < nb) load(ena, ga);
+        consume(enb, gb);
       }
     } else {  // one (wider) batch in flight
       for (int i = 0; i < nb; ++i) {
-        load(i, ena, ga);
-        consume(i, ena, ga);
+        load(ena, ga);
+        consume(ena, ga);
       }
     }
-    for (; cur < NBW; ++cur) flush(warp + cur * kSWarps);  // the remaining bins
+    for (; cb < NBW; ++cb) flush(warp + cb * kSWarps);  // the remaining bins
     __syncthreads();  // z[buf] complete; entry buffer `buf` free
     if (threadIdx.x == 0 && item + 2 * gridDim.x < A.total) stage(item + 2 * gridDim.x, buf);
     // Z^T[j0 + c][b0 + h*32 + lane]: 128-byte row segments per column
