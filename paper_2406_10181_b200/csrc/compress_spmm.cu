@@ -95,10 +95,12 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
   auto item_at = [&](long long item) {
     int mi = 0;
     while (mi + 1 < A.count && item >= A.mat[mi].item_end) ++mi;
-    const long long lt = item - (mi ? A.mat[mi - 1].item_end : 0);
-    const int b0 = static_cast<int>(lt % A.ngroups) * kBG;
+    // 32-bit arithmetic: a matrix has < 2^31 items
+    const int lt = static_cast<int>(item - (mi ? A.mat[mi - 1].item_end : 0));
+    const int tile = lt / A.ngroups;
+    const int b0 = (lt - tile * A.ngroups) * kBG;
     const int elo = __ldg(A.mat[mi].ptr + b0);  // padded table: 64-byte aligned
-    return It{mi, static_cast<int>(lt / A.ngroups) * CT, b0, elo};
+    return It{mi, tile * CT, b0, elo};
   };
   // bulk-copy the CSC entries of an item's 32 bins into entry buffer `b`
   auto stage = [&](long long item, int b) {
