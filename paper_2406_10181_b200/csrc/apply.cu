@@ -321,14 +321,14 @@ __global__ void __launch_bounds__(256) k_build_y_vec(const __grid_constant__ YAr
   int mi = 0;
   while (mi + 1 < A.count && task >= A.mat[mi].task_end) ++mi;
   const YMat& M = A.mat[mi];
-  const long long lt = task - (mi ? A.mat[mi - 1].task_end : 0);
   // task order: (band, column group, a-block), a-block fastest: the warps of
-  // one band share its Q entries in L1
-  const int ab = static_cast<int>(lt % A.ablocks);
-  const long long rest = lt / A.ablocks;
+  // one band share its Q entries in L1.  32-bit decode (< 2^31 tasks per matrix)
+  const int lt = static_cast<int>(task - (mi ? A.mat[mi - 1].task_end : 0));
+  const int rest = lt / A.ablocks;
+  const int ab = lt - rest * A.ablocks;
   constexpr int NG = BN / kYVJ;
-  const int cg = static_cast<int>(rest % NG);
-  const int band = static_cast<int>(rest / NG);
+  const int band = rest / NG;
+  const int cg = rest - band * NG;
   const int d = A.d;
   const int a = ab * 128 + 4 * lane;
   const bool a_ok = a < d;  // d % 4 == 0 (host check)
@@ -474,18 +474,17 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
     // ---------------- W / P-entry producer ----------------
     if (lane == 0) {
       const unsigned long long pol = policy_evict_first();
-      int s = 0;
+      int st = 0, rnd = 0;  // ring stage of the current tile and its wrap count
       for (long long u = blockIdx.x; u < A.units; u += gridDim.x) {
         const Unit U = unit_at(A, u);
         const AMat& M = A.mat[U.mi];
         if (USE_IN && A.pf > S)  // fill the L2 prefetch window beyond the ring
           for (int rb = U.rb0 + S; rb < min(U.rb1, U.rb0 + A.pf); ++rb)
             tma_prefetch_2d(&M.tmap, U.band * BN, rb * TR);
-        for (int rb = U.rb0; rb < U.rb1; ++rb, ++s) {
-          const int st = s % S;
+        for (int rb = U.rb0; rb < U.rb1; ++rb, (++st == S) ? (st = 0, ++rnd) : 0) {
           if (USE_IN && A.pf > S && rb + A.pf < U.rb1)
             tma_prefetch_2d(&M.tmap, U.band * BN, (rb + A.pf) * TR);
-          if (s >= S) mbar_wait(empty + st, ((s / S) - 1) & 1);
+          if (rnd > 0) mbar_wait(empty + st, (rnd - 1) & 1);
           const int r0 = rb * TR;
           const int nrows = min(TR, M.m - r0);
           unsigned char* base = ring + st * A.stage_bytes;
@@ -530,7 +529,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
   const int q0 = gw * RPW + rsub;  // this lane's first row in a tile; rows q0 + v*WPG*RPW
   const unsigned y_lane = smem_addr(smem_raw) + jj * 4u;
   const unsigned ring_s = smem_addr(ring);
-  int s = 0, k = 0;
+  int s = 0, k = 0, st = 0, rnd = 0;  // tile counter, unit counter, stage, wrap count
   for (long long u = blockIdx.x; u < A.units; u += gridDim.x, ++k) {
     const Unit U = unit_at(A, u);
     const AMat& M = A.mat[U.mi];
@@ -539,12 +538,11 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
     Tw* const ocol = static_cast<Tw*>(M.out) + j;  // element offsets below fit in 32 bits
     const int ldo = static_cast<int>(M.ldo);
     mbar_wait(yfull, k & 1);
-    for (int rb = U.rb0; rb < U.rb1; ++rb, ++s) {
+    for (int rb = U.rb0; rb < U.rb1; ++rb, ++s, (++st == S) ? (st = 0, ++rnd) : 0) {
       if (s % kNG != grp) continue;
-      const int st = s % S;
       const int r0 = rb * TR;
       const int nrows = min(TR, M.m - r0);
-      mbar_wait(full + st, (s / S) & 1);
+      mbar_wait(full + st, rnd & 1);
       const unsigned base = ring_s + st * A.stage_bytes;
       const unsigned wq = base + (q0 * BN + jj) * static_cast<unsigned>(sizeof(Tw));
       const unsigned pq = base + A.w_bytes + q0 * KR * 4u;
