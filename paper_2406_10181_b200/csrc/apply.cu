@@ -352,12 +352,15 @@ __global__ void __launch_bounds__(256) k_build_y_vec(const __grid_constant__ YAr
     }
   }
   if (!a_ok) return;
+  const unsigned long long pol_last = policy_evict_last();
   float* base = M.yb + (static_cast<long long>(band) * d + a) * BN + cg * kYVJ;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {  // row a + c of the band block: kYVJ contiguous floats
     float4* o = reinterpret_cast<float4*>(base + c * BN);
 #pragma unroll
-    for (int t = 0; t < kYVJ; t += 4) o[t / 4] = make_float4(y[t][c], y[t + 1][c], y[t + 2][c], y[t + 3][c]);
+    for (int t = 0; t < kYVJ; t += 4)  // evict-last: the apply reads Y right after
+      st_hint_f4(reinterpret_cast<float*>(o + t / 4),
+                 make_float4(y[t][c], y[t + 1][c], y[t + 2][c], y[t + 3][c]), pol_last);
   }
 }
 
@@ -529,6 +532,8 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
   const int q0 = gw * RPW + rsub;  // this lane's first row in a tile; rows q0 + v*WPG*RPW
   const unsigned y_lane = smem_addr(smem_raw) + jj * 4u;
   const unsigned ring_s = smem_addr(ring);
+  // W is written once and not re-read: evict-first keeps the Y blocks in L2
+  const unsigned long long pol_first = policy_evict_first();
   int s = 0, k = 0, st = 0, rnd = 0;  // tile counter, unit counter, stage, wrap count
   for (long long u = blockIdx.x; u < A.units; u += gridDim.x, ++k) {
     const Unit U = unit_at(A, u);
@@ -576,11 +581,11 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
         if (nrows == TR) {  // straight-line: rows interleave freely
           const int stride = kq * ldo;
 #pragma unroll
-          for (int v = 0; v < RPT; ++v) orow[v * stride] = row(v);
+          for (int v = 0; v < RPT; ++v) st_hint(orow + v * stride, row(v), pol_first);
         } else {
 #pragma unroll 1
           for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
-            orow[static_cast<long long>(v) * kq * ldo] = row(v);
+            st_hint(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
         }
       }
       __syncwarp();
