@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--concurrent", type=int, default=0,
+                    help="1: compress and update chains on two streams (schedule.py)")
+    ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
+    ap.add_argument("--sms-update", type=int, default=0, help="lsp_set_sm_budget update SMs")
     return ap.parse_args()
 
 
@@ -322,12 +326,16 @@ def run_ours(args):
 
     def record(ph, li, when):
         if recording[0]:
-            ev[(ph, li)][0 if when == "begin" else 1].record(stream)
+            ev[(ph, li)][0 if when == "begin" else 1].record(torch.cuda.current_stream())
 
     # compress(l) -> all-reduce(S_l) async -> finish(l+1): the all-reduce of layer l
     # overlaps the compress of layer l-1 (paper_2406_10181_b200/schedule.py)
+    lsp.set_sm_budget(args.sms_compress, args.sms_update)
+    streams = None
+    if args.concurrent:
+        streams = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
     sched = LayerSchedule(layers, args.lr, group=dist.group.WORLD if world > 1 else None,
-                          record=record)
+                          record=record, streams=streams)
 
     def one_step(record=False):
         recording[0] = record
@@ -400,6 +408,8 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (%.1f GB of G per rank, streamed once)"
                          % (grad_bytes / 1e9),
                    "parallelism": f"dp{world}",
+                   "streams": ("2 (compress | update, SM budget %d | %d)"
+                               % (args.sms_compress, args.sms_update)) if args.concurrent else "1",
                    "step_hbm_bytes_alg": balg,
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},

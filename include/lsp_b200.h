@@ -95,6 +95,13 @@ int lsp_device_count(int* count);
 /* Number of kernels this library has launched in this process (all handles);
  * used by bench.py to report gpu_launches. */
 uint64_t lsp_launch_count(void);
+/* Process-wide cap on the SMs the persistent kernels of each phase size their
+ * grids for (0 = all SMs): compress_sms for stage 1 of compress, update_sms
+ * for the decompress-and-apply stream.  Lets a caller run the compress of one
+ * layer and the update of another concurrently on two streams (schedule.py,
+ * concurrent mode) without one persistent grid starving the other.  No
+ * reference counterpart (the reference runs these serially on the CPU). */
+int lsp_set_sm_budget(int compress_sms, int update_sms);
 /* Default values of lsp_fit_config (projector.hpp:43-51). */
 lsp_fit_config lsp_fit_config_default(void);
 

@@ -23,6 +23,7 @@ from ._lib import (  # noqa: F401
     lib,
     library_path,
     launch_count,
+    set_sm_budget,
 )
 from .projector import (  # noqa: F401
     AdamState,
@@ -48,5 +49,5 @@ __all__ = [
     "AdamState", "DevicePair", "Layer", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
     "identity_pattern", "init_sparse", "load_projector", "projector_gram", "reproject_state", "maybe_update",
     "save_projector", "step", "subsample_size", "update", "LspError", "InvalidArgument",
-    "NumericError", "IoError", "CudaError", "Layout", "lib", "library_path", "launch_count",
+    "NumericError", "IoError", "CudaError", "Layout", "lib", "library_path", "launch_count", "set_sm_budget",
 ]

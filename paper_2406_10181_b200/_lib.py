@@ -77,6 +77,7 @@ _SIGS = {
     "lsp_version": (_i, []),
     "lsp_device_count": (_i, [_ip]),
     "lsp_launch_count": (C.c_uint64, []),
+    "lsp_set_sm_budget": (_i, [_i, _i]),
     "lsp_fit_config_default": (FitConfigC, []),
     "lsp_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
     "lsp_init_sparse": (_i, [_i, _i, _i, C.c_uint64, _i32p, _dp]),
@@ -175,6 +176,12 @@ class _Lib:
 
 
 lib = _Lib()
+
+
+def set_sm_budget(compress_sms: int = 0, update_sms: int = 0) -> None:
+    """Cap the SMs the persistent compress / update grids size for (0 = all);
+    see lsp_set_sm_budget in include/lsp_b200.h."""
+    lib.set_sm_budget(int(compress_sms), int(update_sms))
 
 
 def launch_count() -> int:

@@ -646,7 +646,7 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
     const int smem = p0.d * 32 * static_cast<int>(sizeof(float)) + kYWarps * 2 * BN * KR * 4;
     auto kern = k_build_y_smem<BN, KR>;
     LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int grid = static_cast<int>(std::min<long long>(units, num_sms()));
+    const int grid = static_cast<int>(std::min<long long>(units, sm_budget(kBudgetUpdate)));
     kern<<<grid, kYWarps * 32, smem, st>>>(B);
     after_launch("build_y_smem");
     return;
@@ -678,7 +678,7 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
   if (A.stages < 3) return false;
   A.pf = 0;  // L2 prefetch distance in tiles (0: off)
   if (const char* e = std::getenv("LSP_APPLY_PF")) A.pf = std::atoi(e);
-  const int grid_max = num_sms();
+  const int grid_max = sm_budget(kBudgetUpdate);
   long long tiles = 0;
   for (const DecJob& J : jobs)
     tiles += static_cast<long long>(ceil_div(J.pr->n, BN)) * ceil_div(J.pr->m, TR);

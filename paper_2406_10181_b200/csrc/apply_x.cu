@@ -370,7 +370,7 @@ bool apply_x_impl(const std::vector<DecJob>& jobs, double alpha, double beta, co
   const int xb_al = static_cast<int>(round_up(A.xb_bytes, 1024));
   A.stages = std::min(8, (kXSmemMax - 1024 - xb_al - bar_bytes) / A.stage_bytes);
   if (A.stages < 3) return false;
-  const int grid_max = num_sms();
+  const int grid_max = sm_budget(kBudgetUpdate);
   long long tiles = 0;
   for (const DecJob& J : jobs)
     tiles += static_cast<long long>(ceil_div(J.pr->m, kXR)) * ceil_div(J.pr->n, kXCols);

@@ -46,6 +46,13 @@ int num_sms() {
   return sms;
 }
 
+std::atomic<int> g_budget[2] = {{0}, {0}};
+
+int sm_budget(int phase) {
+  const int b = g_budget[phase].load(std::memory_order_relaxed);
+  return b > 0 ? std::min(b, num_sms()) : num_sms();
+}
+
 template <typename F>
 int guard(F&& f) {
   try {
@@ -294,6 +301,14 @@ extern "C" {
 const char* lsp_last_error(void) { return g_last_error.c_str(); }
 int lsp_version(void) { return LSP_B200_VERSION; }
 uint64_t lsp_launch_count(void) { return g_launches.load(); }
+
+int lsp_set_sm_budget(int compress_sms, int update_sms) {
+  return guard([&] {
+    if (compress_sms < 0 || update_sms < 0) fail(LSP_EINVAL, "lsp_set_sm_budget: negative budget");
+    g_budget[0].store(compress_sms);
+    g_budget[1].store(update_sms);
+  });
+}
 
 int lsp_device_count(int* count) {
   return guard([&] {

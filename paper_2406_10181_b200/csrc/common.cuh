@@ -53,6 +53,9 @@ inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b
 
 size_t dtype_size(lsp_dtype t);
 int num_sms();
+// SMs a persistent grid of the given phase may size for (lsp_set_sm_budget)
+enum { kBudgetCompress = 0, kBudgetUpdate = 1 };
+int sm_budget(int phase);
 
 #ifdef __CUDACC__
 // ---------------------------------------------------------------------------

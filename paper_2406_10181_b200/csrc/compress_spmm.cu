@@ -303,7 +303,7 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
   if (smem > 227 * 1024) return false;
   auto kern = k_compress_spmm<Tin, Projector::kPadU>;  // U = pad unit
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int grid = static_cast<int>(std::min<long long>(total, kSCtas * num_sms()));
+  const int grid = static_cast<int>(std::min<long long>(total, kSCtas * sm_budget(kBudgetCompress)));
   kern<<<grid, kSThreads, smem, st>>>(A);
   after_launch("compress_spmm");
   return true;

@@ -329,7 +329,7 @@ void decompress_impl(const std::vector<DecJob>& jobs, double alpha, double beta,
   int per_sm = 0;
   LSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem));
   per_sm = std::max(per_sm, 1);
-  const int grid = static_cast<int>(std::min<long long>(total, 1LL * per_sm * num_sms()));
+  const int grid = static_cast<int>(std::min<long long>(total, 1LL * per_sm * sm_budget(kBudgetUpdate)));
   if (nparts) *nparts = grid;
   if (SUMSQ) partials->ensure(static_cast<size_t>(grid) * sizeof(double));
   A.partials = SUMSQ ? partials->as<double>() : nullptr;

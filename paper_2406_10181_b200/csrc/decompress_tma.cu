@@ -354,7 +354,7 @@ bool tma_impl(const std::vector<DecJob>& jobs, double alpha, double beta, const 
   const int smem = L.total();
   auto kern = use_in ? k_decompress_tma<Tw, Tacc, BN, true> : k_decompress_tma<Tw, Tacc, BN, false>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
+  const int grid = static_cast<int>(std::min<long long>(total, sm_budget(kBudgetUpdate)));
   kern<<<grid, kTThreads, smem, st>>>(A);
   after_launch("decompress_tma");
   return true;

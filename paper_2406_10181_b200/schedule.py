@@ -13,7 +13,12 @@ the pipeline is real:
         finish(l+1): wait(S_{l+1}) -> Adam -> W -= lr P dS Q^T
 
 so the all-reduce of layer l overlaps the compress of layer l-1 and the apply of
-layer l+1.  Anything that exposes ``compress()``, ``s_buffer()``, ``adam(check)``
+layer l+1.  With ``streams=(compress_stream, update_stream)`` (concurrent mode)
+the compress chain and the update chain (Adam -> Y build -> W stream) also run
+on two CUDA streams, joined by one event per layer: the compress of layer l-1
+(an L2-gather-latency-bound kernel) overlaps the HBM-bound W update of layer
+l+1 on the device.  ``lsp_set_sm_budget`` sizes the two persistent grids so
+neither starves the other.  Anything that exposes ``compress()``, ``s_buffer()``, ``adam(check)``
 and ``apply(lr)`` can be scheduled: ``paper_2406_10181_b200.Layer`` on the GPU,
 or a CPU stand-in (tests/test_dist_cpu.py runs this exact class over gloo).
 """
@@ -24,7 +29,7 @@ from typing import Callable, Optional, Sequence
 
 class LayerSchedule:
     def __init__(self, layers: Sequence, lr: float, group=None,
-                 record: Optional[Callable[[str, int, str], None]] = None):
+                 record: Optional[Callable[[str, int, str], None]] = None, streams=None):
         """layers: in forward order; group: a torch.distributed process group or
         None for a single rank; record(phase, layer, "begin"|"end") is called
         around every stage (bench.py hangs CUDA events on it)."""
@@ -32,6 +37,8 @@ class LayerSchedule:
         self.lr = lr
         self.group = group
         self.record = record
+        self.streams = streams  # None or (compress stream, update stream), torch.cuda.Stream
+        self._events = None
         self.world = 1
         if group is not None:
             import torch.distributed as dist
@@ -77,6 +84,8 @@ class LayerSchedule:
         return list(reversed(range(len(self.layers))))
 
     def step(self):
+        if self.streams is not None:
+            return self._step_concurrent()
         pending = None
         for li in self.order():
             self._rec("compress", li, "begin")
@@ -88,6 +97,43 @@ class LayerSchedule:
             pending = (li, work)
         if pending is not None:
             self._finish(*pending)
+
+
+    def _step_concurrent(self):
+        import torch
+
+        sc, su = self.streams
+        if self._events is None:
+            self._events = [torch.cuda.Event() for _ in self.layers]
+        main = torch.cuda.current_stream()
+        sc.wait_stream(main)
+        su.wait_stream(main)
+        pending = None
+        for li in self.order():
+            with torch.cuda.stream(sc):
+                self._rec("compress", li, "begin")
+                self.layers[li].compress()
+                self._rec("compress", li, "end")
+                work = self._allreduce(li)
+                ev = None
+                if work is None:
+                    ev = self._events[li]
+                    ev.record(sc)
+            if pending is not None:
+                self._finish_on(su, *pending)
+            pending = (li, work, ev)
+        if pending is not None:
+            self._finish_on(su, *pending)
+        main.wait_stream(sc)
+        main.wait_stream(su)
+
+    def _finish_on(self, su, li, work, ev):
+        import torch
+
+        with torch.cuda.stream(su):
+            if ev is not None:
+                su.wait_event(ev)
+            self._finish(li, work)
 
 
 class _SumThenScale:
