@@ -364,6 +364,30 @@ def test_decompress_y_bitwise_vs_band(cuda, port, monkeypatch):
         assert torch.equal(outs[0], outs[1])
 
 
+def test_build_y_tile_bitwise_vs_vec(cuda, port, monkeypatch):
+    """The shared-memory Y build (k_build_y_t32, opt-in) and the L2-gather build
+    (k_build_y_vec, default) give bitwise-equal W, for ragged n (partial last band and
+    chunk), d = 96 (not a multiple of 64), r = 2, 4, 8 (d = 48 and 16 take the
+    fallback); and match the oracle."""
+    monkeypatch.setenv("LSP_APPLY_ROWS", "0")
+    monkeypatch.setenv("LSP_DECOMPRESS_BAND", "0")
+    for (m, n, d, r) in [(1000, 1500, 256, 4), (300, 2100, 48, 2), (257, 4100, 1024, 4),
+                         (513, 700, 96, 8), (64, 33, 16, 4)]:
+        P, Q, pair = make(port, m, n, d, r, m + 5 * n)
+        delta = f32normal(d + 3, (d, d))
+        w0 = f32normal(n + 3, (m, n), 0.02)
+        outs = []
+        for tile in ("1", "0"):
+            monkeypatch.setenv("LSP_BUILD_Y_TILE", tile)
+            w = dev(w0)
+            pair.decompress_apply(dev(delta), 1e-3, w)
+            outs.append(w)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), (m, n, d, r)
+        ref = port.decompress_apply(P, Q, delta, 1e-3, w0)
+        assert rel(host(outs[0]) - w0, ref - w0) < 1e-5, (m, n, d, r)
+
+
 @pytest.mark.parametrize("rows", ["1", "0"])
 def test_decompress_row_orientation(cuda, port, rows, monkeypatch):  # opt-in path and default
     """The row-orientation apply (apply_x.cu, n > m, fp32): ragged m (not a multiple

@@ -123,6 +123,144 @@ __global__ void ring(const __grid_constant__ RArgs A) {
     }
 }
 
+// ring3: `ring` with clusters of CL CTAs that stream adjacent bands b0..b0+CL-1
+// at the same row blocks in lockstep: before each TMA load the producer
+// arrives (remote mbarrier arrive) on every cluster peer's sync barrier and
+// waits for all CL arrivals on its own, so the CL 128-byte segments of each
+// W row are requested together (a 128*CL-byte span of the row).
+__global__ void ring3(const __grid_constant__ RArgs A) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  unsigned char* rg = sm + A.reserve;
+  unsigned long long* full = (unsigned long long*)(rg + A.stages * A.tile_bytes);
+  unsigned long long* empty = full + A.stages;
+  unsigned long long* sync = empty + A.stages;
+  unsigned cr, CL;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(CL));
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, S = A.stages;
+  const int per_group = A.nc / A.ng;
+  if (tid == 0) { for (int s = 0; s < S; ++s) { mb_init(full + s, 1); mb_init(empty + s, per_group); }
+    mb_init(sync, CL);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  asm volatile("barrier.cluster.arrive.aligned; barrier.cluster.wait.aligned;" ::: "memory");
+  const int nb = (A.n + A.bn - 1) / A.bn, rbs = (A.m + A.tr - 1) / A.tr;
+  if (warp == A.nc) {  // producer
+    if (lane == 0) {
+      unsigned long long pol; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int s = 0;
+      for (int b0 = cid * CL; b0 < nb; b0 += ncl * CL)
+        for (int rb = 0; rb < rbs; ++rb, ++s) {
+          if (!A.tstore) {  // tstore = 1: no lockstep (control)
+          for (unsigned p = 0; p < CL; ++p) {
+            unsigned ra; asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(sa(sync)), "r"(p));
+            asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+          }
+          asm volatile("{\n.reg .pred p;\nW3:\nmbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n@!p bra W3;\n}" ::"r"(sa(sync)), "r"(s & 1) : "memory");
+          }
+          const int b = b0 + cr;
+          if (b >= nb) continue;
+          const int st = s % S;
+          if (s >= S) mb_wait(empty + st, ((s / S) - 1) & 1);
+          mb_expect(full + st, A.tile_bytes);
+          asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+            ::"r"(sa(rg + st * A.tile_bytes)), "l"(&A.map), "r"(b * A.bn), "r"(rb * A.tr), "r"(sa(full + st)), "l"(pol) : "memory");
+        }
+    }
+  } else {
+    const int g = warp / per_group, wg = warp % per_group;
+    const int lanes_per_row = A.bn / 4 < 32 ? A.bn / 4 : 32;
+    const int rows_per_instr = 32 / lanes_per_row;
+    int s = 0;
+    for (int b0 = cid * CL; b0 < nb; b0 += ncl * CL)
+      for (int rb = 0; rb < rbs; ++rb, ++s) {
+        const int b = b0 + cr;
+        if (b >= nb || s % A.ng != g) continue;
+        const int st = s % S;
+        mb_wait(full + st, (s / S) & 1);
+        float* t = (float*)(rg + st * A.tile_bytes);
+        for (int q = wg * rows_per_instr + lane / lanes_per_row; q < A.tr; q += per_group * rows_per_instr) {
+          for (int c4 = lane % lanes_per_row; c4 < A.bn / 4; c4 += lanes_per_row) {
+            float4 v = *(const float4*)(t + q * A.bn + c4 * 4);
+            v.x = 0.999f * v.x + 1e-3f; v.y = 0.999f * v.y + 1e-3f; v.z = 0.999f * v.z + 1e-3f; v.w = 0.999f * v.w + 1e-3f;
+            const int r = rb * A.tr + q, c = b * A.bn + c4 * 4;
+            if (r < A.m && c < A.n) *(float4*)(A.w + (size_t)r * A.n + c) = v;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mb_arrive(empty + st);
+      }
+  }
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.aligned; barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// ring4: clusters of CL CTAs own "super-bands" of CL*32 columns; CTA k of the
+// cluster streams columns [32k, 32k+32) of it.  Only the leader's producer
+// issues loads: per tile CL boxes side by side (one W row segment of CL*128
+// bytes, back to back from one TMA unit), box k multicast to CTA k alone
+// (ctaMask = 1 << k).  Consumers free a stage by a remote arrive on the
+// leader's empty barrier.
+__global__ void ring4(const __grid_constant__ RArgs A) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  unsigned char* rg = sm + A.reserve;
+  unsigned long long* full = (unsigned long long*)(rg + A.stages * A.tile_bytes);
+  unsigned long long* empty = full + A.stages;
+  unsigned cr, CL;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(CL));
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, S = A.stages;
+  const int per_group = A.nc / A.ng;
+  if (tid == 0) { for (int s = 0; s < S; ++s) { mb_init(full + s, 1); mb_init(empty + s, per_group * CL); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  asm volatile("barrier.cluster.arrive.aligned; barrier.cluster.wait.aligned;" ::: "memory");
+  const int sbw = 32 * CL;
+  const int nsb = (A.n + sbw - 1) / sbw, rbs = (A.m + A.tr - 1) / A.tr;
+  if (warp == A.nc) {  // producer
+    if (lane == 0) {
+      unsigned long long pol; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int s = 0;
+      for (int sb = cid; sb < nsb; sb += ncl)
+        for (int rb = 0; rb < rbs; ++rb, ++s) {
+          const int st = s % S;
+          const int ph = (s / S) & 1;
+          if (s >= S) mb_wait(full + st, ph ^ 1);  // own previous phase landed before re-arming
+          mb_expect(full + st, A.tile_bytes);
+          if (cr == 0) {
+            if (s >= S) mb_wait(empty + st, ph ^ 1);
+            for (unsigned k = 0; k < CL; ++k) {
+              const unsigned short mask = (unsigned short)(1u << k);
+              asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;"
+                ::"r"(sa(rg + st * A.tile_bytes)), "l"(&A.map), "r"(sb * sbw + 32 * k), "r"(rb * A.tr), "r"(sa(full + st)), "h"(mask), "l"(pol) : "memory");
+            }
+          }
+        }
+    }
+  } else {
+    const int g = warp / per_group, wg = warp % per_group;
+    unsigned rempty; asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rempty) : "r"(sa(empty)));
+    int s = 0;
+    for (int sb = cid; sb < nsb; sb += ncl)
+      for (int rb = 0; rb < rbs; ++rb, ++s) {
+        if (s % A.ng != g) continue;
+        const int st = s % S;
+        mb_wait(full + st, (s / S) & 1);
+        float* t = (float*)(rg + st * A.tile_bytes);
+        for (int q = wg * 4 + lane / 8; q < A.tr; q += per_group * 4) {
+          float4 v = *(const float4*)(t + q * 32 + (lane % 8) * 4);
+          v.x = 0.999f * v.x + 1e-3f; v.y = 0.999f * v.y + 1e-3f; v.z = 0.999f * v.z + 1e-3f; v.w = 0.999f * v.w + 1e-3f;
+          const int r = rb * A.tr + q, c = sb * sbw + cr * 32 + (lane % 8) * 4;
+          if (r < A.m && c < A.n) *(float4*)(A.w + (size_t)r * A.n + c) = v;
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(rempty + st * 8) : "memory");
+      }
+  }
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.aligned; barrier.cluster.wait.aligned;" ::: "memory");
+}
+
 
 // ring2: tiles of NB boxes side by side (box = 32 fp32 cols x TR rows, 128B
 // swizzle), i.e. a TR x 32*NB tile whose rows are 128*NB bytes of W; lane =
@@ -235,6 +373,42 @@ int main() {
     CK(cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     double gbs = timeit([&] { ring<<<sms, (c.nc + 1) * 32, smem>>>(A); });
     printf("ring bn=%3d tr=%3d S=%2d ng=%d nc=%d reserve=%3dK inflight=%3dK tstore=%d: %.0f GB/s\n", c.bn, c.tr, c.stages, c.ng, c.nc, c.reserve / 1024, c.stages * A.tile_bytes / 1024, c.ts, gbs);
+  }
+  for (int ns : {1, 0}) for (int cl : {1, 2, 4, 8}) for (int tr : {64, 128}) {
+    const int stages = tr == 64 ? 8 : 4;
+    RArgs A{}; A.w = w; A.m = m; A.n = n; A.bn = 32; A.tr = tr; A.stages = stages; A.ng = 2; A.nc = 16; A.reserve = 128 * 1024;
+    A.tile_bytes = 32 * tr * 4; A.tstore = ns;
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m}; cuuint64_t str[1] = {(cuuint64_t)n * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)tr}; cuuint32_t es[2] = {1, 1};
+    if (enc(&A.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode failed\n"); continue; }
+    int smem = A.reserve + stages * A.tile_bytes + 2 * stages * 8 + 16;
+    CK(cudaFuncSetAttribute(ring3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaLaunchConfig_t lc{}; cudaLaunchAttribute at[1];
+    lc.gridDim = dim3(sms / cl * cl); lc.blockDim = dim3(17 * 32); lc.dynamicSmemBytes = smem;
+    at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = cl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    lc.attrs = at; lc.numAttrs = 1;
+    double gbs = timeit([&] { CK(cudaLaunchKernelEx(&lc, ring3, A)); });
+    printf("ring3 lockstep=%d cluster=%d bn=32 tr=%d S=%d ng=2 reserve=128K: %.0f GB/s\n", !ns, cl, tr, stages, gbs);
+  }
+  for (int cl : {1, 2, 4, 8}) for (int tr : {32, 64, 128}) {
+    const int stages = 4 * 128 / tr > 12 ? 12 : 4 * 128 / tr;
+    RArgs A{}; A.w = w; A.m = m; A.n = n; A.bn = 32; A.tr = tr; A.stages = stages; A.ng = 2; A.nc = 16; A.reserve = 128 * 1024;
+    A.tile_bytes = 32 * tr * 4;
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m}; cuuint64_t str[1] = {(cuuint64_t)n * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)tr}; cuuint32_t es[2] = {1, 1};
+    if (enc(&A.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode failed\n"); continue; }
+    int smem = A.reserve + stages * A.tile_bytes + 2 * stages * 8 + 16;
+    CK(cudaFuncSetAttribute(ring4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (cl > 1) CK(cudaFuncSetAttribute(ring4, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t lc{}; cudaLaunchAttribute at[1];
+    lc.blockDim = dim3(17 * 32); lc.dynamicSmemBytes = smem;
+    at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = cl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    lc.attrs = at; lc.numAttrs = 1;
+    lc.gridDim = dim3(sms / cl * cl);
+    int ncl = 0; CK(cudaOccupancyMaxActiveClusters(&ncl, ring4, &lc));
+    lc.gridDim = dim3(ncl * cl);
+    double gbs = timeit([&] { CK(cudaLaunchKernelEx(&lc, ring4, A)); });
+    printf("ring4 multicast cluster=%d (active %d -> %d CTAs) tr=%d S=%d: %.0f GB/s\n", cl, ncl, ncl * cl, tr, stages, gbs);
   }
   return 0;
 }
