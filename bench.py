@@ -60,6 +60,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--profile-out", default=None,
+                    help="write the measured per-layer times as a reference TimingProfile JSON "
+                         "(paper_2406_10181_b200/calibrate.py) for --profile-world ranks")
+    ap.add_argument("--profile-world", type=int, default=8)
+    ap.add_argument("--busbw-gbs", type=float, default=700.0,
+                    help="all-reduce bus bandwidth for --profile-out (nominal NVLink 5 figure; "
+                         "not measured on one GPU)")
     ap.add_argument("--concurrent", type=int, default=0,
                     help="1: compress and update chains on two streams (schedule.py)")
     ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
@@ -432,6 +439,21 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if args.profile_out and rank == 0:
+        from paper_2406_10181_b200 import calibrate as cal
+
+        per_layer = len(items) // L
+        prof = cal.b200_profile([c * 1e-3 for c in comp_ms],
+                                [(a + b + c) * 1e-3 for a, b, c in zip(adam_ms, build_ms, app_ms)],
+                                [per_layer * d * d * 4.0] * L, args.profile_world,
+                                args.busbw_gbs * 1e9)
+        cal.save_profile(prof, args.profile_out)
+        est = cal.step_estimate(prof)
+        line["dp_projection"] = {"world": args.profile_world, "busbw_gbs": args.busbw_gbs,
+                                 "busbw_source": "nominal (one GPU here)",
+                                 "profile": args.profile_out,
+                                 "transition_layer": cal.transition_layer(prof),
+                                 **{k: v for k, v in est.items()}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, _ = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr)
         line["cpu_baseline"] = cb

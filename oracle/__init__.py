@@ -111,6 +111,10 @@ class Oracle:
                                              C.c_char_p, C.c_int64]
             L.ref_time_step.argtypes = pair + [_f64p, _f64p, C.c_double, C.c_int, C.c_int,
                                                C.POINTER(C.c_double)]
+            if hasattr(L, "ref_schedule_eval"):
+                L.ref_schedule_eval.argtypes = [C.c_int, _f64p, C.c_double, C.c_double, C.c_int,
+                                                C.c_double, C.c_int, C.c_int, _f64p]
+                L.ref_schedule_file.argtypes = [C.c_char_p, C.c_int, _f64p]
             L.ref_maybe_update.argtypes = pair + [_f64p, _f64p, C.c_int64, _f64p, C.c_int, _f64p,
                                                   C.c_int, C.c_double, C.c_double, C.c_double,
                                                   C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -230,6 +234,25 @@ class Oracle:
         return out.value
 
     # reference-only helpers
+    def has_schedule(self) -> bool:
+        return self.kind == "reference" and hasattr(self.lib, "ref_schedule_eval")
+
+    def schedule_eval(self, prof, d: int, iters: int = 5) -> dict:
+        """proj/src/schedule_sim.cpp on a calibrate.TimingProfile (ref_capi.cpp)."""
+        out = np.zeros(5)
+        vecs = self._f64(prof.vecs())
+        self._check(self.lib.ref_schedule_eval(prof.n_layers, vecs, prof.bandwidth_d2h,
+                                               prof.bandwidth_h2d, int(prof.duplex),
+                                               prof.bytes_per_element, d, iters, out))
+        return {"transition_layer": out[0], "closed_form_lsp": out[1],
+                "closed_form_zero": out[2], "iter_lsp_layerwise": out[3], "iter_zero": out[4]}
+
+    def schedule_file(self, path: str, iters: int = 5) -> dict:
+        """load_profile + simulate(lsp_layerwise) on a profile JSON file."""
+        out = np.zeros(3)
+        self._check(self.lib.ref_schedule_file(path.encode(), iters, out))
+        return {"n_layers": int(out[0]), "transition_layer": out[1], "iter_lsp_layerwise": out[2]}
+
     def save_projector(self, P: Projector) -> str:
         need = self.lib.ref_save_projector(P.n_rows, P.d, P.r, P.pos, P.val, None, 0)
         buf = C.create_string_buffer(int(need))

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <sstream>
@@ -25,6 +26,9 @@
 #include "lsp/projector.hpp"
 #include "lsp/subspace_opt.hpp"
 #include "lsp/trainer.hpp"
+#ifdef LSP_REF_SCHEDULE
+#include "lsp/schedule_sim.hpp"
+#endif
 
 namespace {
 
@@ -357,3 +361,42 @@ int ref_maybe_update(int m, int n, int d, int r_old, const int32_t* ppos, const 
 }
 
 }  // extern "C"
+
+#ifdef LSP_REF_SCHEDULE
+// proj/src/schedule_sim.cpp: the schedule model on a profile given as arrays
+// (vecs: fwd_gpu, bwd_gpu, upd_gpu, fwd_cpu, bwd_cpu, upd_cpu, grad_bytes,
+// delta_bytes, each n_layers long, concatenated).  out[0] transition_layer
+// (:373-395), out[1] closed_form_lsp(d) (:407-422; NaN when d < 1),
+// out[2] closed_form_zero (:397-405), out[3] simulate(lsp_layerwise, iters)
+// iter_time, out[4] simulate(zero, iters) iter_time.
+extern "C" int ref_schedule_eval(int n_layers, const double* vecs, double bw_d2h, double bw_h2d,
+                                 int duplex, double bytes_per_element, int d, int iters,
+                                 double* out) {
+  return guard([&] {
+    lsp::TimingProfile p;
+    p.n_layers = n_layers;
+    std::vector<double>* fields[] = {&p.fwd_gpu, &p.bwd_gpu, &p.upd_gpu, &p.fwd_cpu,
+                                     &p.bwd_cpu, &p.upd_cpu, &p.grad_bytes, &p.delta_bytes};
+    for (int k = 0; k < 8; ++k) fields[k]->assign(vecs + k * n_layers, vecs + (k + 1) * n_layers);
+    p.bandwidth_d2h = bw_d2h;
+    p.bandwidth_h2d = bw_h2d;
+    p.duplex = duplex != 0;
+    p.bytes_per_element = bytes_per_element;
+    out[0] = lsp::transition_layer(p);
+    out[1] = d >= 1 ? lsp::closed_form_lsp(p, d) : std::nan("");
+    out[2] = lsp::closed_form_zero(p);
+    out[3] = lsp::simulate(p, lsp::Policy::kLspLayerwise, iters).iter_time;
+    out[4] = lsp::simulate(p, lsp::Policy::kZero, iters).iter_time;
+  });
+}
+
+// load_profile (:456-505) on a JSON file, then simulate(lsp_layerwise).
+extern "C" int ref_schedule_file(const char* path, int iters, double* out) {
+  return guard([&] {
+    const lsp::TimingProfile p = lsp::load_profile(path);
+    out[0] = p.n_layers;
+    out[1] = lsp::transition_layer(p);
+    out[2] = lsp::simulate(p, lsp::Policy::kLspLayerwise, iters).iter_time;
+  });
+}
+#endif
