@@ -467,6 +467,7 @@ struct alignas(64) AMat {
   void* out;
   long long ldo;
   int m, n, row_blocks, nbands, rps;  // rps: row blocks per unit (row segment)
+  int nbu;  // units per row segment: nbands, or band pairs for the cluster-pair kernel
   long long unit_end;
 };
 struct AArgs {
@@ -490,9 +491,9 @@ __device__ __forceinline__ Unit unit_at(const AArgs& A, long long u) {
   while (i + 1 < A.count && u >= A.mat[i].unit_end) ++i;
   const AMat& M = A.mat[i];
   const long long lt = u - (i ? A.mat[i - 1].unit_end : 0);
-  const int seg = static_cast<int>(lt / M.nbands);
+  const int seg = static_cast<int>(lt / M.nbu);
   const int rb0 = seg * M.rps;
-  return Unit{i, static_cast<int>(lt % M.nbands), rb0, min(M.row_blocks, rb0 + M.rps)};
+  return Unit{i, static_cast<int>(lt % M.nbu), rb0, min(M.row_blocks, rb0 + M.rps)};
 }
 
 __device__ __forceinline__ float lds_f32(unsigned addr) {
@@ -535,7 +536,13 @@ __device__ __forceinline__ float lds_w(unsigned addr) {
   }
 }
 
-template <typename Tw, int BN, int KR, bool USE_IN>
+// PAIR (opt-in): 2-CTA clusters own pairs of adjacent bands; CTA k of the
+// pair streams band 2u+k.  The leader's producer issues both W boxes of a
+// tile back to back (one 2*BN-column row span of W per request pair, the
+// access pattern tools/micro/stream_rmw.cu ring4 measured faster), each
+// multicast to its CTA alone, and the tile's P entries multicast to both;
+// consumers free a stage with a remote arrive on the leader's empty barrier.
+template <typename Tw, int BN, int KR, bool USE_IN, bool PAIR>
 __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant__ AArgs A) {
   constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
   constexpr int TR = TRW < 256 ? TRW : 256;  // W rows per tile (16 KB of W; <= 256 TMA box rows)
@@ -553,26 +560,59 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = A.stages;
 
+  unsigned crank = 0;
+  if constexpr (PAIR) crank = cluster_ctarank();
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kNC / kNG);
+      mbar_init(empty + s, (PAIR ? 2 : 1) * (kNC / kNG));
     }
     mbar_init(yfull, 1);
     mbar_init(yempty, kNC);
     fence_mbar_init();
   }
-  __syncthreads();
-  if (blockIdx.x >= A.units) return;
+  if constexpr (PAIR) {
+    cluster_sync_all();  // peers' barriers initialised before any remote arrive
+  } else {
+    __syncthreads();
+  }
+  // unit sequence of this CTA (of its cluster for PAIR: both CTAs walk it)
+  const long long u_first = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const long long u_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  if (u_first >= A.units) return;  // PAIR grids never have idle clusters
 
   if (warp == 0) {
     // ---------------- W / P-entry producer ----------------
     if (lane == 0) {
       const unsigned long long pol = policy_evict_first();
       int st = 0, rnd = 0;  // ring stage of the current tile and its wrap count
-      for (long long u = blockIdx.x; u < A.units; u += gridDim.x) {
+      for (long long u = u_first; u < A.units; u += u_step) {
         const Unit U = unit_at(A, u);
         const AMat& M = A.mat[U.mi];
+        if constexpr (PAIR) {
+          for (int rb = U.rb0; rb < U.rb1; ++rb, (++st == S) ? (st = 0, ++rnd) : 0) {
+            if (rnd > 0) {
+              // leader: both CTAs consumed the stage; everyone: own previous
+              // phase complete before re-arming it
+              if (crank == 0) mbar_wait(empty + st, (rnd - 1) & 1);
+              mbar_wait(full + st, (rnd - 1) & 1);
+            }
+            const int r0 = rb * TR;
+            const int nrows = min(TR, M.m - r0);
+            unsigned char* base = ring + st * A.stage_bytes;
+            const unsigned eb = (static_cast<unsigned>(nrows) * KR * 4u + 15u) & ~15u;
+            mbar_arrive_expect_tx(full + st, A.w_bytes + 2u * eb);
+            if (crank == 0) {
+              tma_load_2d_mc(base, &M.tmap, (2 * U.band) * BN, r0, full + st, 1, pol);
+              tma_load_2d_mc(base, &M.tmap, (2 * U.band + 1) * BN, r0, full + st, 2, pol);
+              bulk_load_mc(base + A.w_bytes, M.ppos_scaled + static_cast<long long>(r0) * KR, eb,
+                           full + st, 3);
+              bulk_load_mc(base + A.w_bytes + A.e_bytes, M.pval + static_cast<long long>(r0) * KR,
+                           eb, full + st, 3);
+            }
+          }
+          continue;
+        }
         if (USE_IN && A.pf > S)  // fill the L2 prefetch window beyond the ring
           for (int rb = U.rb0 + S; rb < min(U.rb1, U.rb0 + A.pf); ++rb)
             tma_prefetch_2d(&M.tmap, U.band * BN, rb * TR);
@@ -595,24 +635,26 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
         }
       }
     }
-    return;
-  }
-  if (warp == 1) {
+  } else if (warp == 1) {
     // ---------------- Y block producer (one bulk copy per unit) ----------------
     if (lane == 0) {
       int k = 0;
-      for (long long u = blockIdx.x; u < A.units; u += gridDim.x, ++k) {
+      for (long long u = u_first; u < A.units; u += u_step, ++k) {
         const Unit U = unit_at(A, u);
+        const int band = PAIR ? 2 * U.band + static_cast<int>(crank) : U.band;
         if (k > 0) mbar_wait(yempty, (k - 1) & 1);
+        if (PAIR && band >= A.mat[U.mi].nbands) {  // odd band count: no Y, no stores
+          mbar_arrive(yfull);
+          continue;
+        }
         mbar_arrive_expect_tx(yfull, static_cast<unsigned>(A.y_bytes));
         const unsigned char* src = reinterpret_cast<const unsigned char*>(
-            A.mat[U.mi].yb + static_cast<long long>(U.band) * A.d * BN);
+            A.mat[U.mi].yb + static_cast<long long>(band) * A.d * BN);
         for (int off = 0; off < A.y_bytes; off += kYChunk)
           bulk_load(smem_raw + off, src + off, min(kYChunk, A.y_bytes - off), yfull);
       }
     }
-    return;
-  }
+  } else {
 
   // ---------------- consumers ----------------
   constexpr int WPG = kNC / kNG;          // warps per consumer group
@@ -627,10 +669,11 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
   // W is written once and not re-read: evict-first keeps the Y blocks in L2
   const unsigned long long pol_first = policy_evict_first();
   int s = 0, k = 0, st = 0, rnd = 0;  // tile counter, unit counter, stage, wrap count
-  for (long long u = blockIdx.x; u < A.units; u += gridDim.x, ++k) {
+  for (long long u = u_first; u < A.units; u += u_step, ++k) {
     const Unit U = unit_at(A, u);
     const AMat& M = A.mat[U.mi];
-    const int j = U.band * BN + jj;
+    const int band = PAIR ? 2 * U.band + static_cast<int>(crank) : U.band;
+    const int j = band * BN + jj;
     const bool col_ok = j < M.n;
     Tw* const ocol = static_cast<Tw*>(M.out) + j;  // element offsets below fit in 32 bits
     const int ldo = static_cast<int>(M.ldo);
@@ -681,9 +724,20 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st);
+      if (lane == 0) {
+        if constexpr (PAIR) {
+          mbar_arrive_cluster(empty + st, 0);
+        } else {
+          mbar_arrive(empty + st);
+        }
+      }
     }
     if (lane == 0) mbar_arrive(yempty);  // this unit's Y block may be replaced
+  }
+  }  // consumers
+  if constexpr (PAIR) {
+    __syncwarp();
+    cluster_sync_all();  // no CTA exits while its peer may still signal it
   }
 }
 
@@ -789,10 +843,35 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
   if (A.stages < 3) return false;
   A.pf = 0;  // L2 prefetch distance in tiles (0: off)
   if (const char* e = std::getenv("LSP_APPLY_PF")) A.pf = std::atoi(e);
-  const int grid_max = sm_budget(kBudgetUpdate);
+  const char* pair_env = std::getenv("LSP_APPLY_PAIR");
+  const bool pair = use_in && pair_env && pair_env[0] == '1';
+  const int smem = A.y_bytes + A.stages * A.stage_bytes + bar_bytes;
+  auto kern = pair ? k_apply_y<Tw, BN, KR, true, true>
+                   : (use_in ? k_apply_y<Tw, BN, KR, true, false> : k_apply_y<Tw, BN, KR, false, false>);
+  LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  int grid_max = sm_budget(kBudgetUpdate);
+  if (pair) {  // grid_max counts clusters: as many 2-CTA clusters as fit at once
+    cfg.blockDim = dim3(kAThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(grid_max / 2 * 2);
+    int ncl = 0;
+    LSP_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg));
+    if (ncl < 1) return false;
+    grid_max = std::min(ncl, grid_max / 2);
+  }
   long long tiles = 0;
   for (const DecJob& J : jobs)
-    tiles += static_cast<long long>(ceil_div(J.pr->n, BN)) * ceil_div(J.pr->m, TR);
+    tiles += static_cast<long long>(ceil_div(ceil_div(J.pr->n, BN), pair ? 2 : 1)) *
+             ceil_div(J.pr->m, TR);
   // unit (row segment of a band) at most ~1/4 of a CTA's share, so the
   // round-robin deal stays balanced; env LSP_APPLY_SEG overrides (rows blocks)
   long long cap = std::max<long long>(8, tiles / grid_max / 4);
@@ -813,17 +892,21 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
     M.m = pr.m, M.n = pr.n;
     M.row_blocks = ceil_div(pr.m, TR);
     M.nbands = ceil_div(pr.n, BN);
+    M.nbu = pair ? ceil_div(M.nbands, 2) : M.nbands;
     const int segs = ceil_div(M.row_blocks, cap);
     M.rps = ceil_div(M.row_blocks, segs);
-    units += static_cast<long long>(M.nbands) * ceil_div(M.row_blocks, M.rps);
+    units += static_cast<long long>(M.nbu) * ceil_div(M.row_blocks, M.rps);
     M.unit_end = units;
   }
   A.units = units;
   if (units == 0) return true;
-  const int smem = A.y_bytes + A.stages * A.stage_bytes + bar_bytes;
-  auto kern = use_in ? k_apply_y<Tw, BN, KR, true> : k_apply_y<Tw, BN, KR, false>;
-  LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = static_cast<int>(std::min<long long>(units, grid_max));
+  if (pair) {
+    cfg.gridDim = dim3(2 * grid);
+    LSP_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
+    after_launch("apply_y_pair");
+    return true;
+  }
   kern<<<grid, kAThreads, smem, st>>>(A);
   after_launch("apply_y");
   return true;

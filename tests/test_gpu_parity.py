@@ -364,6 +364,32 @@ def test_decompress_y_bitwise_vs_band(cuda, port, monkeypatch):
         assert torch.equal(outs[0], outs[1])
 
 
+def test_apply_cluster_pair_bitwise(cuda, port, monkeypatch):
+    """The 2-CTA cluster apply (LSP_APPLY_PAIR=1: leader-issued multicast W boxes
+    and P entries, remote stage release) is bitwise equal to the default apply,
+    for even and odd band counts (n = 4100 / 517: the last pair's second CTA has
+    no band), r = 2, 4, 8, fp32 and bf16 W; and matches the oracle."""
+    monkeypatch.setenv("LSP_APPLY_ROWS", "0")
+    monkeypatch.setenv("LSP_DECOMPRESS_BAND", "0")
+    for (m, n, d, r, wdt) in [(1000, 1500, 256, 4, torch.float32), (300, 4100, 1024, 4, torch.float32),
+                              (513, 517, 96, 8, torch.float32), (515, 700, 96, 2, torch.float32),
+                              (1000, 1500, 256, 4, torch.bfloat16), (77, 33, 64, 4, torch.float32)]:
+        P, Q, pair = make(port, m, n, d, r, m + 7 * n)
+        delta = f32normal(d + 5, (d, d))
+        w0 = f32normal(n + 5, (m, n), 0.02)
+        outs = []
+        for pv in ("0", "1"):
+            monkeypatch.setenv("LSP_APPLY_PAIR", pv)
+            w = dev(w0).to(wdt)
+            pair.decompress_apply(dev(delta), 1e-3, w)
+            outs.append(w)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), (m, n, d, r, wdt)
+        if wdt == torch.float32:
+            ref = port.decompress_apply(P, Q, delta, 1e-3, w0)
+            assert rel(host(outs[1]) - w0, ref - w0) < 1e-5, (m, n, d, r)
+
+
 def test_build_y_tile_bitwise_vs_vec(cuda, port, monkeypatch):
     """The shared-memory Y build (k_build_y_t32, opt-in) and the L2-gather build
     (k_build_y_vec, default) give bitwise-equal W, for ragged n (partial last band and
