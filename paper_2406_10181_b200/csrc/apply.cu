@@ -365,97 +365,6 @@ __global__ void __launch_bounds__(256) k_build_y_vec(const __grid_constant__ YAr
 }
 
 
-// Y build with the Delta block staged in shared memory (opt-in,
-// LSP_BUILD_Y_TILE=1): one CTA = (matrix, 32-row block a0 of a, chunk of `cb`
-// bands); Delta^T[:, a0:a0+32] (d rows of 128 B, read once from L2) sits in
-// shared memory.  Lane = a, one column at a time, so each Delta gather is one
-// conflict-free 128-byte row segment; the band's Q entries are staged per
-// warp in shared memory (one coalesced load per lane, prefetched a band
-// ahead) and read as broadcasts.  Same fmaf order as k_build_y_vec, so Y is
-// bitwise identical.  Measured on B200 (C4): 111-117 us per layer vs 101-105
-// for k_build_y_vec (issue-latency bound at 24 warps/SM, and the per-lane
-// 128-byte output rows double the L2 write sectors), so not the default.
-constexpr int kT32Warps = 24;
-template <int KR>
-__global__ void __launch_bounds__(kT32Warps * 32, 1) k_build_y_t32(const __grid_constant__ YArgs A, int cb) {
-  if (A.skip && *A.skip) return;
-  extern __shared__ __align__(16) float dsm[];  // [d][32], then per-warp entries
-  const int d = A.d;
-  int* ep = reinterpret_cast<int*>(dsm + d * 32);
-  float* ev = reinterpret_cast<float*>(ep + kT32Warps * 32 * KR);
-  const int task = static_cast<int>(blockIdx.x);
-  int mi = 0;
-  while (mi + 1 < A.count && task >= A.mat[mi].task_end) ++mi;
-  const YMat& M = A.mat[mi];
-  const int lt = task - static_cast<int>(mi ? A.mat[mi - 1].task_end : 0);
-  const int ch = lt / A.ablocks;
-  const int ab = lt - ch * A.ablocks;
-  const int a0 = ab * 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b1 = min(M.nbands, (ch + 1) * cb);
-  int band = ch * cb + warp;
-  auto load_ent = [&](int b) {
-    Ent<KR> e;
-    const int j = b * 32 + lane;
-    if (b < b1 && j < M.n) {
-      e = ent_ldg<KR>(M.qpos + static_cast<long long>(j) * KR, M.qval + static_cast<long long>(j) * KR);
-    } else {
-#pragma unroll
-      for (int k = 0; k < KR; ++k) e.p[k] = 0, e.v[k] = 0.0f;
-    }
-    return e;
-  };
-  Ent<KR> nxt = load_ent(band);
-  {
-    const float4* src = reinterpret_cast<const float4*>(M.dT + a0);
-    float4* dst = reinterpret_cast<float4*>(dsm);
-    const int tot = d * 8;
-    constexpr int U = 4;
-    for (int i0 = threadIdx.x; i0 < tot; i0 += U * blockDim.x) {
-      float4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i < tot) v[u] = __ldg(src + static_cast<long long>(i >> 3) * (d / 4) + (i & 7));
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i < tot) dst[i] = v[u];
-      }
-    }
-  }
-  __syncthreads();
-  int* wp = ep + warp * 32 * KR;
-  float* wv = ev + warp * 32 * KR;
-  const unsigned long long pol_last = policy_evict_last();
-  for (; band < b1; band += kT32Warps) {
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < KR; ++k) wp[lane * KR + k] = nxt.p[k] * 32, wv[lane * KR + k] = nxt.v[k];
-    __syncwarp();
-    nxt = load_ent(band + kT32Warps);
-    const int jv = M.n - band * 32;  // valid columns in this band
-    float* o = M.yb + (static_cast<long long>(band) * d + a0 + lane) * 32;
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float y[16];
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int c = hh * 16 + t;
-        float acc = 0.0f;
-#pragma unroll
-        for (int k = 0; k < KR; ++k) acc = fmaf(wv[c * KR + k], dsm[wp[c * KR + k] + lane], acc);
-        y[t] = c < jv ? acc : 0.0f;
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        st_hint_f4(o + hh * 16 + 4 * c, make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]),
-                   pol_last);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // streaming apply
 // ---------------------------------------------------------------------------
@@ -774,25 +683,6 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
   A.total = total;
   B.units = units;
   if (total == 0) return;
-  const char* tile_env = std::getenv("LSP_BUILD_Y_TILE");
-  if (BN == 32 && p0.d % 32 == 0 && p0.d * 128 + kT32Warps * 32 * KR * 8 <= 220 * 1024 && tile_env &&
-      tile_env[0] == '1') {
-    int cb = 64;  // bands per CTA
-    if (const char* e = std::getenv("LSP_BUILD_Y_CB")) cb = std::max(1, std::atoi(e));
-    YArgs T = A;
-    T.ablocks = p0.d / 32;
-    long long tt = 0;
-    for (int i = 0; i < T.count; ++i) {
-      tt += static_cast<long long>(T.ablocks) * ceil_div(T.mat[i].nbands, cb);
-      T.mat[i].task_end = tt;
-    }
-    const int smem = p0.d * 128 + kT32Warps * 32 * KR * 8;
-    auto kern = k_build_y_t32<KR>;
-    LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<static_cast<unsigned>(tt), kT32Warps * 32, smem, st>>>(T, cb);
-    after_launch("build_y_t32");
-    return;
-  }
   const char* vec_env = std::getenv("LSP_BUILD_Y_VEC");
   if (p0.d % 4 == 0 && BN % kYVJ == 0 && !(vec_env && vec_env[0] == '0')) {
     YArgs V = A;
