@@ -446,7 +446,7 @@ def run_ours(args):
         prof = cal.b200_profile([c * 1e-3 for c in comp_ms],
                                 [(a + b + c) * 1e-3 for a, b, c in zip(adam_ms, build_ms, app_ms)],
                                 [per_layer * d * d * 4.0] * L, args.profile_world,
-                                args.busbw_gbs * 1e9)
+                                args.busbw_gbs * 1e9, d=d)
         cal.save_profile(prof, args.profile_out)
         est = cal.step_estimate(prof)
         line["dp_projection"] = {"world": args.profile_world, "busbw_gbs": args.busbw_gbs,

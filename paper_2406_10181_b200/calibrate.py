@@ -196,13 +196,18 @@ def step_estimate(p: TimingProfile) -> Dict[str, float]:
 
 def b200_profile(compress_s: Sequence[float], update_s: Sequence[float], s_bytes: Sequence[float],
                  world: int, busbw: float, fwd_s: Optional[Sequence[float]] = None,
-                 bwd_s: Optional[Sequence[float]] = None,
-                 bytes_per_element: float = 4.0) -> TimingProfile:
+                 bwd_s: Optional[Sequence[float]] = None, d: Optional[int] = None) -> TimingProfile:
     """Profile of a measured B200 step (module docstring for the mapping).
     compress_s / update_s: per-layer seconds in FORWARD layer order (update =
     Adam + Y build + apply); s_bytes: bytes of each layer's S buffer; busbw:
     all-reduce bus bandwidth in bytes/s (NCCL's busbw convention, so the ring
-    volume 2(N-1)/N * |S| divided by it is the all-reduce time)."""
+    volume 2(N-1)/N * |S| divided by it is the all-reduce time).
+
+    With ``d`` (and world > 1, equal S sizes per layer) the profile is also
+    invariant under the reference's ``lsp_rescale(profile, d)``, which the
+    ``lspkit sim --policy lsp_layerwise --d`` path applies first: the element
+    width is set so that 2*d^2*bytes_per_element equals the layer's ring bytes,
+    and the upload link is made free (there is no upload on B200)."""
     L = len(compress_s)
     if len(update_s) != L or len(s_bytes) != L:
         raise ValueError("per-layer lists must have equal length")
@@ -211,6 +216,12 @@ def b200_profile(compress_s: Sequence[float], update_s: Sequence[float], s_bytes
     fwd = list(fwd_s) if fwd_s is not None else [0.0] * L
     bwd = list(bwd_s) if bwd_s is not None else [0.0] * L
     ring = 2.0 * (world - 1) / world
+    bytes_per_element, bw_up = 4.0, float(busbw)
+    if d is not None and world > 1:
+        if len(set(float(b) for b in s_bytes)) != 1:
+            raise ValueError("rescale-invariant profile needs equal S bytes per layer")
+        bytes_per_element = ring * float(s_bytes[0]) / (2.0 * float(d) * float(d))
+        bw_up = 1e18
     prof = TimingProfile(
         n_layers=L,
         fwd_gpu=[float(x) for x in fwd],
@@ -219,7 +230,7 @@ def b200_profile(compress_s: Sequence[float], update_s: Sequence[float], s_bytes
         fwd_cpu=[0.0] * L, bwd_cpu=[0.0] * L, upd_cpu=[0.0] * L,
         grad_bytes=[ring * float(b) for b in s_bytes],
         delta_bytes=[0.0] * L,
-        bandwidth_d2h=float(busbw), bandwidth_h2d=float(busbw), duplex=True,
+        bandwidth_d2h=float(busbw), bandwidth_h2d=bw_up, duplex=True,
         mem_total=0.0, mem_gpu=0.0, bytes_per_element=float(bytes_per_element))
     prof.validate()
     return prof

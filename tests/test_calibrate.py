@@ -87,3 +87,19 @@ def test_b200_profile_runs_in_reference_simulator(tmp_path, world):
     if world == 1:
         assert est["allreduce_s"] == 0.0
         assert sim["iter_lsp_layerwise"] == pytest.approx(est["device_s"], rel=1e-9)
+
+
+def test_b200_profile_rescale_invariant():
+    """With d given, the reference CLI path (lsp_rescale before simulate, as
+    lspkit sim --policy lsp_layerwise --d does) sees the same link times."""
+    ref = _ref()
+    L, d = 16, 1024
+    prof = cal.b200_profile([0.35e-3] * L, [0.49e-3] * L, [7 * d * d * 4.0] * L, 8, 700e9,
+                            bwd_s=[0.4e-3] * L, d=d)
+    resc = cal.lsp_rescale(prof, d)
+    assert resc.grad_bytes == pytest.approx(prof.grad_bytes, rel=1e-12)
+    a = ref.schedule_eval(prof, d)
+    b = ref.schedule_eval(resc, d)
+    assert b["iter_lsp_layerwise"] == pytest.approx(a["iter_lsp_layerwise"], rel=1e-9)
+    # the rescaled upload (payload / 1e18 B/s) adds ~1e-10 s
+    assert a["closed_form_lsp"] == pytest.approx(cal.closed_form_b200(prof), rel=1e-6)
