@@ -1,0 +1,73 @@
+"""GPU: LayerSchedule modes and launch knobs leave results bitwise unchanged.
+
+* concurrent mode (compress chain and update chain on two streams, one event
+  per layer) vs the default single-stream schedule;
+* lsp_set_sm_budget (smaller persistent grids for the compress and the apply)
+  vs all SMs -- the kernels' work partition changes, their arithmetic order
+  per element does not.
+"""
+import pytest
+import torch
+
+import paper_2406_10181_b200 as lsp
+from paper_2406_10181_b200.schedule import LayerSchedule
+
+pytestmark = pytest.mark.gpu
+KINIT = 0x1A171
+SHAPES = [(512, 512), (512, 1376), (1376, 512)]
+D, R, L = 128, 4, 4
+
+
+def _build(seed=5):
+    layers, ws = [], []
+    k = 0
+    g = torch.Generator(device="cuda")
+    for _ in range(L):
+        pairs, bound = [], []
+        for (m, n) in SHAPES:
+            P = lsp.DeviceProjector.random(m, D, R, lsp.derive_seed(seed, KINIT, 2 * k))
+            Q = lsp.DeviceProjector.random(n, D, R, lsp.derive_seed(seed, KINIT, 2 * k + 1))
+            pairs.append(lsp.DevicePair(P, Q))
+            g.manual_seed(100 + k)
+            bound.append((torch.randn(m, n, device="cuda", generator=g),
+                          0.02 * torch.randn(m, n, device="cuda", generator=g)))
+            k += 1
+        lay = lsp.Layer(pairs)
+        for i, (gi, wi) in enumerate(bound):
+            lay.bind(i, gi, wi)
+        layers.append(lay)
+        ws.extend(w for _, w in bound)
+    return layers, ws
+
+
+def _run(streams=None, budget=(0, 0), steps=3):
+    lsp.set_sm_budget(*budget)
+    try:
+        layers, ws = _build()
+        sched = LayerSchedule(layers, 1e-3, streams=streams)
+        for _ in range(steps):
+            sched.step()
+        torch.cuda.synchronize()
+        return [w.clone() for w in ws]
+    finally:
+        lsp.set_sm_budget(0, 0)
+
+
+def test_concurrent_streams_bitwise(cuda):
+    ref = _run()
+    got = _run(streams=(torch.cuda.Stream(), torch.cuda.Stream()))
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("budget", [(16, 0), (0, 10), (37, 61)])
+def test_sm_budget_bitwise(cuda, budget):
+    ref = _run()
+    got = _run(budget=budget)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+
+
+def test_sm_budget_rejects_negative():
+    with pytest.raises(lsp.LspError):
+        lsp.set_sm_budget(-1, 0)
