@@ -1,4 +1,8 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_schedule.py tests/test_gpu_dp.py -q -x 2>&1 | tail -3
-timeout 600 python bench.py --no-cpu-baseline --no-e2e --profile-out gpurun_out/c4_timing_profile.json > gpurun_out/b.json 2>gpurun_out/b.err; python -c "
-import json;d=json.load(open('gpurun_out/b.json'));print(d['ms_per_step'], d['dp_projection'])" || tail -3 gpurun_out/b.err
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "compress" 2>&1 | tail -2
+b() { timeout 300 python bench.py --config $1 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b.json 2>gpurun_out/b.err; python -c "
+import json;d=json.load(open('gpurun_out/b.json'));b=d['breakdown'];print('$1 $2', 'ms/step',round(d['ms_per_step'],2),{k:round(v,2) for k,v in b.items() if k.endswith('ms_per_step')})" || tail -3 gpurun_out/b.err; }
+b c4 ctas3
+b c4-bf16 ctas3
+b c3 ctas3
+b c2 ctas3
