@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--busbw-gbs", type=float, default=700.0,
                     help="all-reduce bus bandwidth for --profile-out (nominal NVLink 5 figure; "
                          "not measured on one GPU)")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1 (default): capture one step in a CUDA graph and replay it in the "
+                         "timed region (N=1 only; the per-phase split comes from one eager "
+                         "step just before); 0: eager launches")
     ap.add_argument("--concurrent", type=int, default=0,
                     help="1: compress and update chains on two streams (schedule.py)")
     ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
@@ -352,6 +356,17 @@ def run_ours(args):
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
+    graph, graph_launches = None, 0
+    if args.graph and world == 1:
+        one_step(record=True)  # per-phase split (eager), outside the timed region
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        g0 = lsp.launch_count()
+        with torch.cuda.graph(graph):
+            sched.step()
+        graph_launches = lsp.launch_count() - g0
+        graph.replay()  # warm the graph once
+        torch.cuda.synchronize()
 
     # ---- timed region -------------------------------------------------------
     clocks = Clocks(local)
@@ -365,12 +380,15 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for k in range(args.steps):
-        one_step(record=(k == args.steps - 1))
+        if graph is not None:
+            graph.replay()
+        else:
+            one_step(record=(k == args.steps - 1))
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = lsp.launch_count() - launches0
+    launches = lsp.launch_count() - launches0 + graph_launches * (args.steps if graph else 0)
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
     comp_ms = [ev[("compress", li)][0].elapsed_time(ev[("compress", li)][1]) for li in range(L)]
@@ -415,6 +433,9 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (%.1f GB of G per rank, streamed once)"
                          % (grad_bytes / 1e9),
                    "parallelism": f"dp{world}",
+                   "cuda_graph": (("one captured step replayed per timed step; phase split "
+                                   "and roofline launch times from one eager step before it")
+                                  if graph is not None else False),
                    "streams": ("2 (compress | update, SM budget %d | %d)"
                                % (args.sms_compress, args.sms_update)) if args.concurrent else "1",
                    "step_hbm_bytes_alg": balg,

@@ -71,3 +71,30 @@ def test_sm_budget_bitwise(cuda, budget):
 def test_sm_budget_rejects_negative():
     with pytest.raises(lsp.LspError):
         lsp.set_sm_budget(-1, 0)
+
+
+def test_cuda_graph_replay_bitwise(cuda):
+    """bench.py's default timed loop: one captured LayerSchedule step replayed;
+    the device-side Adam step counter advances per replay, so eager steps and
+    replays give bitwise-equal weights and moments."""
+    ref_layers, ref_ws = _build()
+    s1 = LayerSchedule(ref_layers, 1e-3)
+    for _ in range(4):
+        s1.step()
+    layers, ws = _build()
+    s2 = LayerSchedule(layers, 1e-3)
+    s2.step()  # eager: allocates the lazily-sized workspaces
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        s2.step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ref_ws, ws):
+        assert torch.equal(a, b)
+    for la, lb in zip(ref_layers, layers):
+        ma, va, sa = la.adam_get(0)
+        mb, vb, sb = lb.adam_get(0)
+        assert sa == sb == 4
+        assert (ma == mb).all() and (va == vb).all()
