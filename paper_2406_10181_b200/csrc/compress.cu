@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
   const Tin* __restrict__ g = static_cast<const Tin*>(M.g);
   const Ent* __restrict__ ent = static_cast<const Ent*>(M.ent);
   const int* __restrict__ split = M.split;
-  const int d = A.d, m = M.m, n = M.n, bm = A.bm, r = A.r;
+  const int d = A.d, m = M.m, n = M.n, bm = A.bm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j0 = band * 32;
   const int bin0 = blockIdx.y * NT + warp * 32;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_compress_stage1(const __grid_
                    : "=r"(o0), "=r"(w0), "=r"(o1), "=r"(w1) : "r"(ep));
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
-        const unsigned ep_end = e_base + static_cast<unsigned>(__shfl_sync(0xffffffffu, my_end, b)) * 8u;
+        unsigned ep_end = e_base + static_cast<unsigned>(__shfl_sync(0xffffffffu, my_end, b)) * 8u;
         float a = acc[b];
         asm volatile(
             "{\n\t.reg .pred p;\n\t.reg .b32 a0, a1;\n\t.reg .f32 v0, v1, g0, g1;\n"

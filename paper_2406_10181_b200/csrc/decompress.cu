@@ -346,12 +346,6 @@ static bool force_generic() {
   return e && e[0] == '1';
 }
 
-// LSP_DECOMPRESS_BAND=1 skips the Y-precompute path (builds Y_band in-kernel).
-static bool force_band() {
-  const char* e = std::getenv("LSP_DECOMPRESS_BAND");
-  return e && e[0] == '1';
-}
-
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st) {
