@@ -435,6 +435,27 @@ __device__ __forceinline__ float4 lds_v4f(unsigned addr) {
   return v;
 }
 template <typename Tw>
+__device__ __forceinline__ float2 lds_w2(unsigned addr) {
+  if constexpr (std::is_same<Tw, float>::value) {
+    return lds_v2f(addr);
+  } else {
+    unsigned h;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(h) : "r"(addr));
+    return make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u));
+  }
+}
+__device__ __forceinline__ void st_hint2(float* a, float2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(a), "f"(v.x), "f"(v.y),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint2(bf16* a, float2 v, unsigned long long pol) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;\n" ::"l"(a),
+               "r"(*reinterpret_cast<const unsigned*>(&h)), "l"(pol)
+               : "memory");
+}
+template <typename Tw>
 __device__ __forceinline__ float lds_w(unsigned addr) {
   if constexpr (std::is_same<Tw, float>::value) {
     return lds_f32(addr);
@@ -451,11 +472,15 @@ __device__ __forceinline__ float lds_w(unsigned addr) {
 // access pattern tools/micro/stream_rmw.cu ring4 measured faster), each
 // multicast to its CTA alone, and the tile's P entries multicast to both;
 // consumers free a stage with a remote arrive on the leader's empty barrier.
-template <typename Tw, int BN, int KR, bool USE_IN, bool PAIR>
+// CPL = 2: each lane owns two adjacent columns (8-byte Y gathers, W loads and
+// stores of two elements), halving the consumer instructions per element;
+// per-element arithmetic unchanged, so results are bitwise equal to CPL = 1.
+template <typename Tw, int BN, int KR, bool USE_IN, bool PAIR, int CPL>
 __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant__ AArgs A) {
   constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
   constexpr int TR = TRW < 256 ? TRW : 256;  // W rows per tile (16 KB of W; <= 256 TMA box rows)
-  constexpr int RPW = 32 / BN;         // rows per warp instruction
+  constexpr int LPR = BN / CPL;        // lanes per W row
+  constexpr int RPW = 32 / LPR;        // rows per warp instruction
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (A.skip && *A.skip) return;
   // consumer warps form kNG groups; group g takes tiles g, g+kNG, ... so kNG
@@ -571,7 +596,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
   const int cw = warp - 2;
   const int grp = cw / WPG, gw = cw % WPG;
   const float alpha = static_cast<float>(A.alpha), beta = static_cast<float>(A.beta);
-  const int jj = lane % BN, rsub = lane / BN;
+  const int jj = (lane % LPR) * CPL, rsub = lane / LPR;
   const int q0 = gw * RPW + rsub;  // this lane's first row in a tile; rows q0 + v*WPG*RPW
   const unsigned y_lane = smem_addr(smem_raw) + jj * 4u;
   const unsigned ring_s = smem_addr(ring);
@@ -584,6 +609,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
     const int band = PAIR ? 2 * U.band + static_cast<int>(crank) : U.band;
     const int j = band * BN + jj;
     const bool col_ok = j < M.n;
+    const bool pair_ok = j + 1 < M.n;  // CPL = 2: both columns in range
     Tw* const ocol = static_cast<Tw*>(M.out) + j;  // element offsets below fit in 32 bits
     const int ldo = static_cast<int>(M.ldo);
     mbar_wait(yfull, k & 1);
@@ -613,23 +639,57 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
             vv[l] = b.x, vv[l + 1] = b.y, vv[l + 2] = b.z, vv[l + 3] = b.w;
           }
         }
-        float acc = vv[0] * lds_f32(y_lane + pp[0]);
+        if constexpr (CPL == 1) {
+          float acc = vv[0] * lds_f32(y_lane + pp[0]);
 #pragma unroll
-        for (int l = 1; l < KR; ++l) acc = fmaf(vv[l], lds_f32(y_lane + pp[l]), acc);
-        float res = alpha * acc;
-        if (USE_IN) res = fmaf(beta, lds_w<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw))), res);
-        return cvt<Tw>(res);
+          for (int l = 1; l < KR; ++l) acc = fmaf(vv[l], lds_f32(y_lane + pp[l]), acc);
+          float res = alpha * acc;
+          if (USE_IN) res = fmaf(beta, lds_w<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw))), res);
+          return cvt<Tw>(res);
+        } else {
+          float2 y0 = lds_v2f(y_lane + pp[0]);
+          float acc0 = vv[0] * y0.x, acc1 = vv[0] * y0.y;
+#pragma unroll
+          for (int l = 1; l < KR; ++l) {
+            const float2 y = lds_v2f(y_lane + pp[l]);
+            acc0 = fmaf(vv[l], y.x, acc0);
+            acc1 = fmaf(vv[l], y.y, acc1);
+          }
+          float r0v = alpha * acc0, r1v = alpha * acc1;
+          if (USE_IN) {
+            const float2 w = lds_w2<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw)));
+            r0v = fmaf(beta, w.x, r0v);
+            r1v = fmaf(beta, w.y, r1v);
+          }
+          return make_float2(r0v, r1v);
+        }
       };
       if (col_ok) {
         Tw* const orow = ocol + static_cast<long long>(r0 + q0) * ldo;
-        if (nrows == TR) {  // straight-line: rows interleave freely
-          const int stride = kq * ldo;
+        if constexpr (CPL == 1) {
+          if (nrows == TR) {  // straight-line: rows interleave freely
+            const int stride = kq * ldo;
 #pragma unroll
-          for (int v = 0; v < RPT; ++v) st_hint(orow + v * stride, row(v), pol_first);
-        } else {
+            for (int v = 0; v < RPT; ++v) st_hint(orow + v * stride, row(v), pol_first);
+          } else {
+#pragma unroll 1
+            for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
+              st_hint(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
+          }
+        } else if (pair_ok) {
+          if (nrows == TR) {
+            const int stride = kq * ldo;
+#pragma unroll
+            for (int v = 0; v < RPT; ++v) st_hint2(orow + v * stride, row(v), pol_first);
+          } else {
+#pragma unroll 1
+            for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
+              st_hint2(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
+          }
+        } else {  // last column of an odd n: first element only
 #pragma unroll 1
           for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
-            st_hint(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
+            st_hint(orow + static_cast<long long>(v) * kq * ldo, cvt<Tw>(row(v).x), pol_first);
         }
       }
       __syncwarp();
@@ -736,8 +796,16 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
   const char* pair_env = std::getenv("LSP_APPLY_PAIR");
   const bool pair = use_in && pair_env && pair_env[0] == '1';
   const int smem = A.y_bytes + A.stages * A.stage_bytes + bar_bytes;
-  auto kern = pair ? k_apply_y<Tw, BN, KR, true, true>
-                   : (use_in ? k_apply_y<Tw, BN, KR, true, false> : k_apply_y<Tw, BN, KR, false, false>);
+  // two columns per lane (default) when every row start is 2-element aligned;
+  // measured on B200: C4 apply 10.6 vs 11.4 ms per step, C4-bf16 7.5 vs 9.5,
+  // C3 1.8 vs 2.2.  LSP_APPLY_CPL=1 forces one column per lane.
+  const char* cpl_env = std::getenv("LSP_APPLY_CPL");
+  bool cpl2 = !(cpl_env && cpl_env[0] == '1');
+  for (const DecJob& J : jobs)
+    cpl2 = cpl2 && J.ldo % 2 == 0 && reinterpret_cast<uintptr_t>(J.out) % (2 * sizeof(Tw)) == 0;
+  auto kern = pair ? k_apply_y<Tw, BN, KR, true, true, 1>
+                   : (use_in ? (cpl2 ? k_apply_y<Tw, BN, KR, true, false, 2> : k_apply_y<Tw, BN, KR, true, false, 1>)
+                             : (cpl2 ? k_apply_y<Tw, BN, KR, false, false, 2> : k_apply_y<Tw, BN, KR, false, false, 1>));
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];

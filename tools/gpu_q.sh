@@ -1,7 +1,5 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "two_columns or decompress or pair" 2>&1 | tail -2
 b() { timeout 300 python bench.py --config $1 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline $3 > gpurun_out/b.json 2>gpurun_out/b.err; python -c "
 import json;d=json.load(open('gpurun_out/b.json'));b=d['breakdown'];print('$1 $2', 'ms/step',round(d['ms_per_step'],3),{k:round(v,2) for k,v in b.items() if k.endswith('ms_per_step')})" || tail -3 gpurun_out/b.err; }
-for c in c2 c3 c4 c4-bf16; do b $c pdl ""; LSP_PDL=0 b $c nopdl ""; done
-b c4 pdl-eager "--graph 0"
-LSP_PDL=0 b c4 nopdl-eager "--graph 0"
+for c in c4 c4-bf16 c3 c2; do b $c cpl1 ""; LSP_APPLY_CPL=2 b $c cpl2 ""; done
