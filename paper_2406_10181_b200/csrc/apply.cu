@@ -434,26 +434,65 @@ __device__ __forceinline__ float4 lds_v4f(unsigned addr) {
                : "r"(addr));
   return v;
 }
-template <typename Tw>
-__device__ __forceinline__ float2 lds_w2(unsigned addr) {
-  if constexpr (std::is_same<Tw, float>::value) {
-    return lds_v2f(addr);
+template <int N>
+struct FV {
+  float v[N];
+};
+template <int N>
+__device__ __forceinline__ FV<N> lds_yv(unsigned addr) {
+  FV<N> r;
+  if constexpr (N == 2) {
+    const float2 t = lds_v2f(addr);
+    r.v[0] = t.x, r.v[1] = t.y;
   } else {
+    const float4 t = lds_v4f(addr);
+    r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+  }
+  return r;
+}
+template <typename Tw, int N>
+__device__ __forceinline__ FV<N> lds_wv(unsigned addr) {
+  FV<N> r;
+  if constexpr (std::is_same<Tw, float>::value) {
+    r = lds_yv<N>(addr);
+  } else if constexpr (N == 2) {
     unsigned h;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(h) : "r"(addr));
-    return make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u));
+    r.v[0] = __uint_as_float(h << 16), r.v[1] = __uint_as_float(h & 0xffff0000u);
+  } else {
+    unsigned h0, h1;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(h0), "=r"(h1) : "r"(addr));
+    r.v[0] = __uint_as_float(h0 << 16), r.v[1] = __uint_as_float(h0 & 0xffff0000u);
+    r.v[2] = __uint_as_float(h1 << 16), r.v[3] = __uint_as_float(h1 & 0xffff0000u);
+  }
+  return r;
+}
+template <int N>
+__device__ __forceinline__ void st_hintv(float* a, const FV<N>& x, unsigned long long pol) {
+  if constexpr (N == 2) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(a), "f"(x.v[0]),
+                 "f"(x.v[1]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(a),
+                 "f"(x.v[0]), "f"(x.v[1]), "f"(x.v[2]), "f"(x.v[3]), "l"(pol)
+                 : "memory");
   }
 }
-__device__ __forceinline__ void st_hint2(float* a, float2 v, unsigned long long pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(a), "f"(v.x), "f"(v.y),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_hint2(bf16* a, float2 v, unsigned long long pol) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;\n" ::"l"(a),
-               "r"(*reinterpret_cast<const unsigned*>(&h)), "l"(pol)
-               : "memory");
+template <int N>
+__device__ __forceinline__ void st_hintv(bf16* a, const FV<N>& x, unsigned long long pol) {
+  const __nv_bfloat162 h0 = __floats2bfloat162_rn(x.v[0], x.v[1]);
+  if constexpr (N == 2) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;\n" ::"l"(a),
+                 "r"(*reinterpret_cast<const unsigned*>(&h0)), "l"(pol)
+                 : "memory");
+  } else {
+    const __nv_bfloat162 h1 = __floats2bfloat162_rn(x.v[2], x.v[3]);
+    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;\n" ::"l"(a),
+                 "r"(*reinterpret_cast<const unsigned*>(&h0)),
+                 "r"(*reinterpret_cast<const unsigned*>(&h1)), "l"(pol)
+                 : "memory");
+  }
 }
 template <typename Tw>
 __device__ __forceinline__ float lds_w(unsigned addr) {
@@ -472,9 +511,10 @@ __device__ __forceinline__ float lds_w(unsigned addr) {
 // access pattern tools/micro/stream_rmw.cu ring4 measured faster), each
 // multicast to its CTA alone, and the tile's P entries multicast to both;
 // consumers free a stage with a remote arrive on the leader's empty barrier.
-// CPL = 2: each lane owns two adjacent columns (8-byte Y gathers, W loads and
-// stores of two elements), halving the consumer instructions per element;
-// per-element arithmetic unchanged, so results are bitwise equal to CPL = 1.
+// CPL = 2 / 4: each lane owns CPL adjacent columns (8- / 16-byte Y gathers, W
+// loads and stores of CPL elements), cutting the consumer instructions per
+// element; per-element arithmetic unchanged, so results are bitwise equal to
+// CPL = 1.
 template <typename Tw, int BN, int KR, bool USE_IN, bool PAIR, int CPL>
 __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant__ AArgs A) {
   constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
@@ -609,7 +649,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
     const int band = PAIR ? 2 * U.band + static_cast<int>(crank) : U.band;
     const int j = band * BN + jj;
     const bool col_ok = j < M.n;
-    const bool pair_ok = j + 1 < M.n;  // CPL = 2: both columns in range
+    const bool group_ok = j + CPL <= M.n;  // all CPL columns of the lane in range
     Tw* const ocol = static_cast<Tw*>(M.out) + j;  // element offsets below fit in 32 bits
     const int ldo = static_cast<int>(M.ldo);
     mbar_wait(yfull, k & 1);
@@ -647,21 +687,23 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
           if (USE_IN) res = fmaf(beta, lds_w<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw))), res);
           return cvt<Tw>(res);
         } else {
-          float2 y0 = lds_v2f(y_lane + pp[0]);
-          float acc0 = vv[0] * y0.x, acc1 = vv[0] * y0.y;
+          FV<CPL> acc = lds_yv<CPL>(y_lane + pp[0]);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc.v[c] = vv[0] * acc.v[c];
 #pragma unroll
           for (int l = 1; l < KR; ++l) {
-            const float2 y = lds_v2f(y_lane + pp[l]);
-            acc0 = fmaf(vv[l], y.x, acc0);
-            acc1 = fmaf(vv[l], y.y, acc1);
+            const FV<CPL> y = lds_yv<CPL>(y_lane + pp[l]);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc.v[c] = fmaf(vv[l], y.v[c], acc.v[c]);
           }
-          float r0v = alpha * acc0, r1v = alpha * acc1;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc.v[c] = alpha * acc.v[c];
           if (USE_IN) {
-            const float2 w = lds_w2<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw)));
-            r0v = fmaf(beta, w.x, r0v);
-            r1v = fmaf(beta, w.y, r1v);
+            const FV<CPL> w = lds_wv<Tw, CPL>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw)));
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc.v[c] = fmaf(beta, w.v[c], acc.v[c]);
           }
-          return make_float2(r0v, r1v);
+          return acc;
         }
       };
       if (col_ok) {
@@ -676,20 +718,24 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
             for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
               st_hint(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
           }
-        } else if (pair_ok) {
+        } else if (group_ok) {
           if (nrows == TR) {
             const int stride = kq * ldo;
 #pragma unroll
-            for (int v = 0; v < RPT; ++v) st_hint2(orow + v * stride, row(v), pol_first);
+            for (int v = 0; v < RPT; ++v) st_hintv<CPL>(orow + v * stride, row(v), pol_first);
           } else {
 #pragma unroll 1
             for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
-              st_hint2(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
+              st_hintv<CPL>(orow + static_cast<long long>(v) * kq * ldo, row(v), pol_first);
           }
-        } else {  // last column of an odd n: first element only
+        } else {  // the last columns of n: the valid ones only
 #pragma unroll 1
-          for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v)
-            st_hint(orow + static_cast<long long>(v) * kq * ldo, cvt<Tw>(row(v).x), pol_first);
+          for (int v = 0; v < RPT && q0 + v * kq < nrows; ++v) {
+            const FV<CPL> x = row(v);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+              if (j + c < M.n) st_hint(orow + static_cast<long long>(v) * kq * ldo + c, cvt<Tw>(x.v[c]), pol_first);
+          }
         }
       }
       __syncwarp();
@@ -790,22 +836,38 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
   const int bar_bytes = (2 * kMaxStages + 2) * 8;
   A.stages = std::min(kMaxStages, (kSmemMax - A.y_bytes - bar_bytes) / A.stage_bytes);
   if (const char* e = std::getenv("LSP_APPLY_STAGES")) A.stages = std::min(A.stages, std::atoi(e));
+  // Group g consumes tiles g, g + kNG, ...: with a stage count that is a
+  // multiple of kNG each stage belongs to one group, so a group's waits on a
+  // stage's full barrier are one phase apart.  With an odd count the groups
+  // share stages, and a fast group can be two phases ahead of a stage whose
+  // parity then matches an older completed phase (it would read stale data).
+  A.stages -= A.stages % kNG;
   if (A.stages < 3) return false;
   A.pf = 0;  // L2 prefetch distance in tiles (0: off)
   if (const char* e = std::getenv("LSP_APPLY_PF")) A.pf = std::atoi(e);
   const char* pair_env = std::getenv("LSP_APPLY_PAIR");
   const bool pair = use_in && pair_env && pair_env[0] == '1';
   const int smem = A.y_bytes + A.stages * A.stage_bytes + bar_bytes;
-  // two columns per lane (default) when every row start is 2-element aligned;
-  // measured on B200: C4 apply 10.6 vs 11.4 ms per step, C4-bf16 7.5 vs 9.5,
-  // C3 1.8 vs 2.2.  LSP_APPLY_CPL=1 forces one column per lane.
+  // columns per lane: 4 by default (2 or 1 when rows are not 4-element
+  // aligned).  Measured on B200, apply ms per step at CPL 1 / 2 / 4: C4
+  // 11.4 / 10.6 / 10.4, C4-bf16 9.5 / 7.5 / 6.8, C3 2.2 / 1.8 / 1.6.
+  // LSP_APPLY_CPL=1|2|4 overrides.
   const char* cpl_env = std::getenv("LSP_APPLY_CPL");
-  bool cpl2 = !(cpl_env && cpl_env[0] == '1');
+  int cpl = cpl_env ? std::atoi(cpl_env) : 4;
+  if (cpl != 1 && cpl != 2 && cpl != 4) cpl = 4;
   for (const DecJob& J : jobs)
-    cpl2 = cpl2 && J.ldo % 2 == 0 && reinterpret_cast<uintptr_t>(J.out) % (2 * sizeof(Tw)) == 0;
-  auto kern = pair ? k_apply_y<Tw, BN, KR, true, true, 1>
-                   : (use_in ? (cpl2 ? k_apply_y<Tw, BN, KR, true, false, 2> : k_apply_y<Tw, BN, KR, true, false, 1>)
-                             : (cpl2 ? k_apply_y<Tw, BN, KR, false, false, 2> : k_apply_y<Tw, BN, KR, false, false, 1>));
+    while (cpl > 1 && (J.ldo % cpl != 0 || reinterpret_cast<uintptr_t>(J.out) % (cpl * sizeof(Tw)) != 0))
+      cpl /= 2;
+  void (*kern)(AArgs);
+  if (pair) {
+    kern = k_apply_y<Tw, BN, KR, true, true, 1>;
+  } else if (use_in) {
+    kern = cpl == 4 ? k_apply_y<Tw, BN, KR, true, false, 4>
+                    : (cpl == 2 ? k_apply_y<Tw, BN, KR, true, false, 2> : k_apply_y<Tw, BN, KR, true, false, 1>);
+  } else {
+    kern = cpl == 4 ? k_apply_y<Tw, BN, KR, false, false, 4>
+                    : (cpl == 2 ? k_apply_y<Tw, BN, KR, false, false, 2> : k_apply_y<Tw, BN, KR, false, false, 1>);
+  }
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];

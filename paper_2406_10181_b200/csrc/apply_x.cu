@@ -369,6 +369,7 @@ bool apply_x_impl(const std::vector<DecJob>& jobs, double alpha, double beta, co
   const int bar_bytes = (2 * 8 + 2) * 8;
   const int xb_al = static_cast<int>(round_up(A.xb_bytes, 1024));
   A.stages = std::min(8, (kXSmemMax - 1024 - xb_al - bar_bytes) / A.stage_bytes);
+  A.stages -= A.stages % kXNG;  // one group per stage (see apply.cu, stage parity)
   if (A.stages < 3) return false;
   const int grid_max = sm_budget(kBudgetUpdate);
   long long tiles = 0;

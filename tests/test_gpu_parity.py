@@ -392,20 +392,23 @@ def test_apply_cluster_pair_bitwise(cuda, port, monkeypatch):
 
 @pytest.mark.parametrize("beta_in", [True, False])
 def test_apply_two_columns_per_lane_bitwise(cuda, port, monkeypatch, beta_in):
-    """k_apply_y with two columns per lane (LSP_APPLY_CPL=2: 8-byte Y gathers and
-    two-element W loads/stores) is bitwise equal to one column per lane, for odd
-    n (last column alone), ragged m, r = 2, 4, 8, fp32 and bf16 W, in-place apply
-    and decompress-only output."""
+    """k_apply_y with two or four columns per lane (LSP_APPLY_CPL=2/4: 8/16-byte Y
+    gathers, multi-element W loads/stores) is bitwise equal to one column per
+    lane, for n not a multiple of 2 or 4 (partial last group), ragged m,
+    r = 2, 4, 8, fp32 and bf16 W, in-place apply and decompress-only output."""
     monkeypatch.setenv("LSP_APPLY_ROWS", "0")
     monkeypatch.setenv("LSP_DECOMPRESS_BAND", "0")
     for (m, n, d, r, wdt) in [(1000, 1500, 256, 4, torch.float32), (300, 4100, 1024, 4, torch.float32),
                               (513, 517, 96, 8, torch.float32), (515, 701, 96, 2, torch.float32),
-                              (1000, 1501, 256, 4, torch.bfloat16), (77, 33, 64, 4, torch.bfloat16)]:
+                              (1000, 1501, 256, 4, torch.bfloat16), (77, 33, 64, 4, torch.bfloat16),
+                              (200, 1002, 128, 4, torch.float32), (130, 4098, 1024, 4, torch.bfloat16),
+                              (600, 1000, 96, 2, torch.float32), (600, 1000, 1024, 2, torch.bfloat16),
+                              (300, 1000, 256, 8, torch.float32)]:
         P, Q, pair = make(port, m, n, d, r, m + 11 * n)
         delta = dev(f32normal(d + 9, (d, d)))
         w0 = f32normal(n + 9, (m, n), 0.02)
         outs = []
-        for cpl in ("1", "2"):
+        for cpl in ("1", "2", "4"):
             monkeypatch.setenv("LSP_APPLY_CPL", cpl)
             if beta_in:
                 w = dev(w0).to(wdt)
@@ -414,7 +417,7 @@ def test_apply_two_columns_per_lane_bitwise(cuda, port, monkeypatch, beta_in):
                 w = pair.decompress(delta, dtype=wdt)
             outs.append(w)
         torch.cuda.synchronize()
-        assert torch.equal(outs[0], outs[1]), (m, n, d, r, wdt, beta_in)
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), (m, n, d, r, wdt, beta_in)
 
 
 @pytest.mark.parametrize("kind", ["smem", "global"])

@@ -98,3 +98,40 @@ def test_cuda_graph_replay_bitwise(cuda):
         mb, vb, sb = lb.adam_get(0)
         assert sa == sb == 4
         assert (ma == mb).all() and (va == vb).all()
+
+
+@pytest.mark.parametrize("d,r", [(1024, 2), (256, 4)])
+def test_graph_replay_back_to_back_full_size(cuda, d, r):
+    """Regression: back-to-back graph replays of a full-size (4096 x 11008) step
+    with r = 2 (d = 1024) or d = 256 -- ring stage counts that came out odd, so
+    the two consumer groups of the streaming apply shared stages and a fast
+    group could pass a stage's parity wait one phase early (stale tile, launch
+    failure).  Replays must match eager steps bitwise."""
+    m, n = 4096, 11008
+
+    def build():
+        P = lsp.DeviceProjector.random(m, d, r, lsp.derive_seed(7, KINIT, 0))
+        Q = lsp.DeviceProjector.random(n, d, r, lsp.derive_seed(7, KINIT, 1))
+        lay = lsp.Layer([lsp.DevicePair(P, Q)])
+        g = torch.Generator(device="cuda")
+        g.manual_seed(11)
+        gm = torch.randn(m, n, device="cuda", generator=g)
+        w = 0.02 * torch.randn(m, n, device="cuda", generator=g)
+        lay.bind(0, gm, w)
+        return lay, gm, w
+
+    la, ga, wa = build()
+    sa = LayerSchedule([la], 1e-3)
+    for _ in range(8):
+        sa.step()
+    lb, gb, wb = build()
+    sb = LayerSchedule([lb], 1e-3)
+    sb.step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        sb.step()
+    for _ in range(7):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(wa, wb)
