@@ -842,7 +842,7 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
   // share stages, and a fast group can be two phases ahead of a stage whose
   // parity then matches an older completed phase (it would read stale data).
   A.stages -= A.stages % kNG;
-  if (A.stages < 3) return false;
+  if (A.stages < kNG) return false;
   A.pf = 0;  // L2 prefetch distance in tiles (0: off)
   if (const char* e = std::getenv("LSP_APPLY_PF")) A.pf = std::atoi(e);
   const char* pair_env = std::getenv("LSP_APPLY_PAIR");
@@ -860,7 +860,8 @@ bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, cons
       cpl /= 2;
   void (*kern)(AArgs);
   if (pair) {
-    kern = k_apply_y<Tw, BN, KR, true, true, 1>;
+    kern = cpl == 4 ? k_apply_y<Tw, BN, KR, true, true, 4>
+                    : (cpl == 2 ? k_apply_y<Tw, BN, KR, true, true, 2> : k_apply_y<Tw, BN, KR, true, true, 1>);
   } else if (use_in) {
     kern = cpl == 4 ? k_apply_y<Tw, BN, KR, true, false, 4>
                     : (cpl == 2 ? k_apply_y<Tw, BN, KR, true, false, 2> : k_apply_y<Tw, BN, KR, true, false, 1>);
