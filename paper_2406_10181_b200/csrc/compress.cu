@@ -433,42 +433,68 @@ struct S2Args {
   int* flag;
 };
 
-constexpr int kS2Threads = 256;
+constexpr int kS2Threads = 128;
+constexpr int kS2V = 2;  // float4 column chunks per thread (d = 1024: the whole row)
 
+// One CTA = one row b of S^T for one matrix: S^T[b][:] = sum over the CSC
+// entries e of Q's column b (ascending row order) of q_e * Z^T[row_e][:].
+// Each thread owns kS2V float4 chunks of the row, so every entry's index and
+// value loads serve 8 columns and 2*4 Z^T loads are in flight per batch.
 __global__ void __launch_bounds__(kS2Threads) k_stage2_f4(const __grid_constant__ S2Args A) {
   const S2Mat& M = A.mat[blockIdx.y];
   const int b = blockIdx.x, d = A.d;
   const int e0 = __ldg(M.ptr + b), e1 = __ldg(M.ptr + b + 1);
   bool bad = false;
-  for (int a0 = 4 * threadIdx.x; a0 < d; a0 += 4 * kS2Threads) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int a_base = 4 * threadIdx.x; a_base < d; a_base += 4 * kS2Threads * kS2V) {
+    float4 acc[kS2V];
+    bool ok[kS2V];
+#pragma unroll
+    for (int c = 0; c < kS2V; ++c) {
+      acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      ok[c] = a_base + c * 4 * kS2Threads < d;
+    }
     int e = e0;
     for (; e + 4 <= e1; e += 4) {
-      float4 z[4];
+      float4 z[4][kS2V];
       float q[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         q[u] = __ldg(M.val + e + u);
-        z[u] = __ldg(reinterpret_cast<const float4*>(M.zt + static_cast<long long>(__ldg(M.row + e + u)) * M.ldz + a0));
+        const float* zr = M.zt + static_cast<long long>(__ldg(M.row + e + u)) * M.ldz + a_base;
+#pragma unroll
+        for (int c = 0; c < kS2V; ++c)
+          z[u][c] = ok[c] ? __ldg(reinterpret_cast<const float4*>(zr + c * 4 * kS2Threads))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc.x = fmaf(q[u], z[u].x, acc.x);
-        acc.y = fmaf(q[u], z[u].y, acc.y);
-        acc.z = fmaf(q[u], z[u].z, acc.z);
-        acc.w = fmaf(q[u], z[u].w, acc.w);
-      }
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < kS2V; ++c) {
+          acc[c].x = fmaf(q[u], z[u][c].x, acc[c].x);
+          acc[c].y = fmaf(q[u], z[u][c].y, acc[c].y);
+          acc[c].z = fmaf(q[u], z[u][c].z, acc[c].z);
+          acc[c].w = fmaf(q[u], z[u][c].w, acc[c].w);
+        }
     }
     for (; e < e1; ++e) {
       const float q = __ldg(M.val + e);
-      const float4 z = __ldg(reinterpret_cast<const float4*>(M.zt + static_cast<long long>(__ldg(M.row + e)) * M.ldz + a0));
-      acc.x = fmaf(q, z.x, acc.x);
-      acc.y = fmaf(q, z.y, acc.y);
-      acc.z = fmaf(q, z.z, acc.z);
-      acc.w = fmaf(q, z.w, acc.w);
+      const float* zr = M.zt + static_cast<long long>(__ldg(M.row + e)) * M.ldz + a_base;
+#pragma unroll
+      for (int c = 0; c < kS2V; ++c) {
+        if (!ok[c]) continue;
+        const float4 z = __ldg(reinterpret_cast<const float4*>(zr + c * 4 * kS2Threads));
+        acc[c].x = fmaf(q, z.x, acc[c].x);
+        acc[c].y = fmaf(q, z.y, acc[c].y);
+        acc[c].z = fmaf(q, z.z, acc[c].z);
+        acc[c].w = fmaf(q, z.w, acc[c].w);
+      }
     }
-    bad |= !(isfinite(acc.x) && isfinite(acc.y) && isfinite(acc.z) && isfinite(acc.w));
-    *reinterpret_cast<float4*>(M.s_t + static_cast<long long>(b) * d + a0) = acc;
+#pragma unroll
+    for (int c = 0; c < kS2V; ++c) {
+      if (!ok[c]) continue;
+      bad |= !(isfinite(acc[c].x) && isfinite(acc[c].y) && isfinite(acc[c].z) && isfinite(acc[c].w));
+      *reinterpret_cast<float4*>(M.s_t + static_cast<long long>(b) * d + a_base + c * 4 * kS2Threads) = acc[c];
+    }
   }
   if (A.flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(A.flag, 1);
 }
