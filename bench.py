@@ -47,6 +47,12 @@ CONFIGS = {
 BYTES = {"f32": 4, "bf16": 2, "f64": 8}
 
 
+def dtype_label(gdt, wdt):
+    """Arithmetic type of the step's big streams (G read, W read-modify-write);
+    S/M/V and every accumulation are fp32 regardless."""
+    return gdt if gdt == wdt else f"g={gdt},w={wdt}"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -424,7 +430,7 @@ def run_ours(args):
         "metric": "grad GB/s (compress+decompress+apply)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(gdt, wdt),
         "data": "synthetic (torch.randn gradients/weights in HBM; projectors from the reference "
                 "trainer seed path)",
         "config": {"workload": desc, "matrices": len(items), "layers": L, "d": d, "r": r,

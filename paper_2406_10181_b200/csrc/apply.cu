@@ -365,6 +365,81 @@ __global__ void __launch_bounds__(256) k_build_y_vec(const __grid_constant__ YAr
 }
 
 
+// Tiled form of k_build_y_vec for BN = 32 (the default Y build): one CTA = 8
+// warps = (matrix, band, 256-row super-block of a); warp w computes column
+// group w % 4 (8 of the band's 32 columns) for a-block w / 4 (128 rows) with
+// exactly k_build_y_vec's loads and FMA order (so Y is bitwise the same), then
+// stages its 128 x 8 outputs in a shared-memory copy of the CTA's output chunk
+// Yb[band][a0 .. a0+255][0 .. 31] -- which is ONE contiguous 32 KB span of
+// the workspace -- and the CTA writes the chunk out with 512-byte coalesced
+// stores.  Stage-in granules are 16 bytes, XOR-swizzled by bits 2..4 of the
+// row so the 8 lanes of a store phase hit 8 distinct bank groups; the
+// write-out reads whole 128-byte rows (conflict-free).  k_build_y_vec wrote
+// 32-byte row pieces straight from the lanes: 8x the L1 store wavefronts.
+constexpr int kYTRows = 256;
+template <int KR>
+__global__ void __launch_bounds__(256) k_build_y_tile(const __grid_constant__ YArgs A) {
+  constexpr int BN = 32;
+  __shared__ __align__(16) float tile[kYTRows * BN];  // 32 KB
+  if (A.skip && *A.skip) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long task = blockIdx.x;  // (matrix, band, super-block), super-block fastest
+  int mi = 0;
+  while (mi + 1 < A.count && task >= A.mat[mi].task_end) ++mi;
+  const YMat& M = A.mat[mi];
+  const int lt = static_cast<int>(task - (mi ? A.mat[mi - 1].task_end : 0));
+  const int band = lt / A.ablocks;   // A.ablocks = super-blocks per band here
+  const int sb = lt - band * A.ablocks;
+  const int d = A.d;
+  const int cg = warp & 3, ab = warp >> 2;
+  const int al = ab * 128 + 4 * lane;  // first of this lane's 4 rows within the chunk
+  const int a = sb * kYTRows + al;
+  const bool a_ok = a < d;  // d % 4 == 0 (host check)
+  float y[kYVJ][4];
+#pragma unroll
+  for (int t = 0; t < kYVJ; ++t) {
+    y[t][0] = y[t][1] = y[t][2] = y[t][3] = 0.0f;
+    const int j = band * BN + cg * kYVJ + t;
+    if (j < M.n) {
+      const Ent<KR> en = ent_ldg<KR>(M.qpos + static_cast<long long>(j) * KR,
+                                     M.qval + static_cast<long long>(j) * KR);
+#pragma unroll
+      for (int e = 0; e < KR; ++e) {
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a_ok) x = __ldg(reinterpret_cast<const float4*>(M.dT + static_cast<long long>(en.p[e]) * d + a));
+        y[t][0] = fmaf(en.v[e], x.x, y[t][0]);
+        y[t][1] = fmaf(en.v[e], x.y, y[t][1]);
+        y[t][2] = fmaf(en.v[e], x.z, y[t][2]);
+        y[t][3] = fmaf(en.v[e], x.w, y[t][3]);
+      }
+    }
+  }
+  // stage: row al + c, granules 2*cg + h (4 floats each) of the row's 8,
+  // physical granule = g ^ ((row >> 2) & 7)
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int row = al + c;
+    const int key = (row >> 2) & 7;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = (2 * cg + h) ^ key;
+      *reinterpret_cast<float4*>(tile + row * BN + 4 * g) =
+          make_float4(y[4 * h][c], y[4 * h + 1][c], y[4 * h + 2][c], y[4 * h + 3][c]);
+    }
+  }
+  __syncthreads();
+  // write-out: rows a0 .. a0 + rows - 1 of the band block are contiguous
+  const int rows = min(kYTRows, d - sb * kYTRows);
+  const unsigned long long pol_last = policy_evict_last();
+  float* out = M.yb + (static_cast<long long>(band) * d + sb * kYTRows) * BN;
+  for (int gi = threadIdx.x; gi < rows * (BN / 4); gi += blockDim.x) {
+    const int row = gi >> 3, g = gi & 7;
+    const float4 v = *reinterpret_cast<const float4*>(tile + row * BN + 4 * (g ^ ((row >> 2) & 7)));
+    st_hint_f4(out + 4 * gi, v, pol_last);  // evict-last: the apply reads Y right after
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // streaming apply
 // ---------------------------------------------------------------------------
@@ -761,7 +836,8 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
   const std::vector<DecJob>& jobs = jobs_in;
   const Pair& p0 = *jobs[0].pr;
   const char* env = std::getenv("LSP_BUILD_Y_GLOBAL");
-  const bool use_smem = p0.d <= kDsMaxD && !(env && env[0] == '1');
+  // the shared-memory build stages Delta^T rows with 16-byte loads: d % 4 == 0
+  const bool use_smem = p0.d <= kDsMaxD && p0.d % 4 == 0 && !(env && env[0] == '1');
   YArgs A{};
   Y2Args B{};
   A.count = B.count = static_cast<int>(jobs.size());
@@ -790,6 +866,22 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
   B.units = units;
   if (total == 0) return;
   const char* vec_env = std::getenv("LSP_BUILD_Y_VEC");
+  const char* tile_env = std::getenv("LSP_BUILD_Y_TILE");
+  if constexpr (BN == 32) {
+    if (p0.d % 4 == 0 && !(vec_env && vec_env[0] == '0') && !(tile_env && tile_env[0] == '0')) {
+      YArgs V = A;
+      V.ablocks = ceil_div(p0.d, kYTRows);  // super-blocks per band
+      long long tv = 0;
+      for (int i = 0; i < V.count; ++i) {
+        tv += static_cast<long long>(V.mat[i].nbands) * V.ablocks;
+        V.mat[i].task_end = tv;
+      }
+      V.total = tv;
+      k_build_y_tile<KR><<<static_cast<unsigned>(tv), 256, 0, st>>>(V);
+      after_launch("build_y_tile");
+      return;
+    }
+  }
   if (p0.d % 4 == 0 && BN % kYVJ == 0 && !(vec_env && vec_env[0] == '0')) {
     YArgs V = A;
     V.ablocks = ceil_div(p0.d, 128);
@@ -994,6 +1086,8 @@ static bool y_eligible(const DecJob& J, lsp_dtype dt, double beta) {
   if ((r != 2 && r != 4 && r != 8) || pr.q->r != r) return false;
   if (pr.d * 8 * 4 > kYMaxBytes) return false;
   if (static_cast<long long>(pr.m) * J.ldo >= (1LL << 31)) return false;  // 32-bit offsets
+  // the Y builds read delta^T with 16-byte vector loads
+  if (reinterpret_cast<uintptr_t>(J.delta_t) % 16) return false;
   if (beta != 0.0) {
     const size_t es = dtype_size(dt);
     if (J.in == nullptr || reinterpret_cast<uintptr_t>(J.in) % 16 || (J.ldi * es) % 16) return false;

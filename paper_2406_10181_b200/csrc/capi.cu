@@ -72,8 +72,10 @@ int guard(F&& f) {
 
 // ---- Projector ---------------------------------------------------------------
 static void upload(DevBuf& b, const void* src, size_t bytes) {
-  b.ensure(bytes + 16);  // 16 bytes of slack: 16-byte bulk copies may round up past the end
+  b.ensure(bytes + 16);  // 16 bytes of slack: 16-byte vector/bulk reads may round up past the end
   if (bytes) LSP_CUDA(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
+  // zero the slack: a vector read that rounds past the end sees position 0 / value 0
+  LSP_CUDA(cudaMemset(static_cast<char*>(b.p) + bytes, 0, b.bytes - bytes));
 }
 
 template <typename T>

@@ -24,7 +24,7 @@
 #include <type_traits>
 
 #include "core.cuh"
-#include "tma.cuh"
+#include "tma.cuh"  // mbarrier / bulk-copy helpers
 
 namespace lspb {
 
@@ -35,19 +35,18 @@ constexpr int kSWarps = 8;   // warps per CTA
 constexpr int kSCtas = 2;    // CTAs per SM: one streams while the other syncs/transposes
 constexpr int kSThreads = kSWarps * 32;
 
-struct alignas(64) PMat {
-  CUtensorMap tmap;     // G, box CT columns x prow rows (L2 prefetch only)
+struct PMat {
   const void* g;
   long long ldg;
   const int* ptr;       // CSC_P offsets [d + 1]
   const EntryF* ent;    // CSC_P entries {row, value}
   float* zt;
-  int ldz, n, ntiles, prow;
+  int ldz, n, ntiles;
   long long item_end;
 };
 struct PArgs {
   PMat mat[kMaxGroup];
-  int count, d, ngroups, ebuf_bytes, pf_items;
+  int count, d, ngroups, ebuf_bytes;
   long long total;
 };
 
@@ -277,20 +276,11 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
     M.ldz = pr.ldz();
     M.n = pr.n;
     M.ntiles = ceil_div(pr.n, CT);
-    M.prow = ceil_div(pr.m, A.ngroups);
-    if (M.prow > 256 || !cached_tmap(&M.tmap, J.g, std::is_same<Tin, float>::value ? LSP_F32 : LSP_BF16,
-                                      pr.m, pr.n, J.ldg, CT, M.prow))
-      M.prow = 0;
     total += static_cast<long long>(M.ntiles) * A.ngroups;
     M.item_end = total;
   }
   A.total = total;
   if (total == 0) return true;
-  int pf_tiles = 8;  // L2 prefetch distance in column tiles (env LSP_SPMM_PF, 0 = off)
-  if (const char* e = std::getenv("LSP_SPMM_PF")) pf_tiles = std::atoi(e);
-  for (int i = 0; i < A.count; ++i)
-    if (A.mat[i].prow == 0) pf_tiles = 0;
-  A.pf_items = pf_tiles * A.ngroups;
   // entry buffer: the largest 32-bin CSC range of any matrix (+16 B alignment slack)
   int emax = 0;
   for (const S1Job& J : jobs) {

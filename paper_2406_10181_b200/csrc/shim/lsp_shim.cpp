@@ -419,16 +419,22 @@ void save_projector(const SparseProjector& p, std::ostream& out) {
   out << buf.c_str();
 }
 SparseProjector load_projector(std::istream& in) {
-  // Consume exactly one projector record: header line plus n_rows lines.
-  std::string header;
-  if (!std::getline(in, header)) throw IoError("load_projector: bad header");
-  std::string text = header + "\n";
+  // Whitespace-token based like the reference (proj/src/projector.cpp:329-354):
+  // consume the three header tokens, then exactly n_rows * 2r value tokens,
+  // whatever the line breaks; the C-ABI parser validates them.
+  std::string h0, h1, h2;
+  if (!(in >> h0 >> h1 >> h2)) throw IoError("load_projector: bad header");
+  std::string text = h0 + ' ' + h1 + ' ' + h2 + '\n';
   int n_rows = 0, d = 0, r = 0;
   int rc = lsp_load_projector(text.c_str(), static_cast<int64_t>(text.size()), &n_rows, &d, &r,
                               nullptr, nullptr);
   if (rc) raise(rc);
-  std::string line;
-  for (int i = 0; i < n_rows && std::getline(in, line); ++i) text += line + "\n";
+  const long long tokens = 2LL * n_rows * r;
+  std::string tok;
+  for (long long t = 0; t < tokens && (in >> tok); ++t) {
+    text += tok;
+    text += ((t + 1) % (2 * r) == 0) ? '\n' : ' ';
+  }
   SparseProjector p;
   p.n_rows = n_rows;
   p.d = d;

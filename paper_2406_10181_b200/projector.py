@@ -185,6 +185,8 @@ class DeviceProjector:
 
     def set_values(self, val):
         val = _np_f64(val)
+        if val.size < self.n_rows * self.r:
+            raise InvalidArgument("projector set_values: array shorter than n_rows * r")
         lib.projector_set_values(self._h, _dptr(val))
 
     def close(self):
@@ -253,6 +255,11 @@ class DevicePair:
         gp, ldg = _check_dev(g, "compress: g", self.m, self.n)
         if out is None:
             out = torch.empty(self.d, self.d, dtype=self._sd(), device=g.device)
+        else:
+            _check_dev(out, "compress: out", self.d, self.d)
+            if out.dtype != self._sd() or not out.is_contiguous():
+                raise InvalidArgument("compress: out must be a contiguous d x d tensor of the "
+                                      "pair's compute dtype")
         lib.compress(self._h, C.c_void_p(gp), ldg, int(_dtype_of(g)), C.c_void_p(out.data_ptr()),
                      int(layout), _stream(stream))
         return out

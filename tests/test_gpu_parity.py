@@ -420,23 +420,25 @@ def test_apply_two_columns_per_lane_bitwise(cuda, port, monkeypatch, beta_in):
         assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), (m, n, d, r, wdt, beta_in)
 
 
-@pytest.mark.parametrize("kind", ["smem", "global"])
+@pytest.mark.parametrize("kind", ["smem", "global", "vec"])
 def test_build_y_variants_bitwise(cuda, port, monkeypatch, kind):
-    """The Y builds staging Delta in shared memory (k_build_y_smem) or gathering
-    it per element (k_build_y) give W bitwise equal to the default L2-gather
-    build (k_build_y_vec), for ragged n, d = 96 (not a multiple of 64), r = 2,
-    4, 8; and match the oracle."""
+    """The Y builds staging Delta in shared memory (k_build_y_smem), gathering
+    it per element (k_build_y) or writing lane-sized row pieces (k_build_y_vec)
+    give W bitwise equal to the default tiled build (k_build_y_tile, coalesced
+    32 KB chunks), for ragged n, d = 96 (not a multiple of 64), d = 1000 (a
+    partial 256-row chunk), r = 2, 4, 8; and match the oracle."""
     monkeypatch.setenv("LSP_APPLY_ROWS", "0")
     monkeypatch.setenv("LSP_DECOMPRESS_BAND", "0")
     for (m, n, d, r) in [(1000, 1500, 256, 4), (300, 2100, 64, 2), (257, 4100, 1024, 4),
-                         (513, 700, 96, 8)]:
+                         (513, 700, 96, 8), (300, 999, 1000, 4)]:
         P, Q, pair = make(port, m, n, d, r, m + 5 * n)
         delta = f32normal(d + 3, (d, d))
         w0 = f32normal(n + 3, (m, n), 0.02)
         outs = []
-        for vec in ("1", "0"):
-            monkeypatch.setenv("LSP_BUILD_Y_VEC", vec)
-            monkeypatch.setenv("LSP_BUILD_Y_GLOBAL", "1" if kind == "global" else "0")
+        for alt in (False, True):
+            monkeypatch.setenv("LSP_BUILD_Y_TILE", "0" if alt and kind == "vec" else "1")
+            monkeypatch.setenv("LSP_BUILD_Y_VEC", "0" if alt and kind != "vec" else "1")
+            monkeypatch.setenv("LSP_BUILD_Y_GLOBAL", "1" if alt and kind == "global" else "0")
             w = dev(w0)
             pair.decompress_apply(dev(delta), 1e-3, w)
             outs.append(w)
