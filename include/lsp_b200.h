@@ -48,7 +48,8 @@ typedef enum {
   LSP_ENUMERIC = 2, /* lsp::NumericError */
   LSP_EIO = 3,      /* lsp::IoError */
   LSP_ECUDA = 4,    /* CUDA runtime failure (incl. no device) */
-  LSP_ENOMEM = 5
+  LSP_ENOMEM = 5,
+  LSP_ENCCL = 6     /* NCCL missing or failed (lsp_comm_*, *_allreduce) */
 } lsp_status;
 
 typedef enum { LSP_F64 = 0, LSP_F32 = 1, LSP_BF16 = 2 } lsp_dtype;
@@ -268,6 +269,34 @@ int lsp_layer_check(lsp_layer_t layer, lsp_stream_t stream);
 /* SYNCHRONOUS host copy of matrix idx's moments and the shared step. */
 int lsp_layer_adam_get(lsp_layer_t layer, int idx, double* m, double* v, int64_t* step,
                        lsp_layout layout);
+
+/* ----------------------------------------------------------------------------
+ * Data-parallel exchange (SURVEY 8(b) lsp_allreduce_S, 8(e)).  The reference
+ * steps one process (proj/src/trainer.cpp:186-198: compress -> adam_step ->
+ * apply per layer); across ranks only S is exchanged, between compress and
+ * Adam: mean(S_rank) == compress(mean G_rank) by linearity
+ * (proj/tests/test_projector.cpp:208-235).  The library owns the NCCL
+ * communicator; NCCL is loaded at run time (libnccl.so.2, reusing a copy
+ * already in the process, e.g. PyTorch's).
+ * -------------------------------------------------------------------------- */
+#define LSP_COMM_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+typedef struct lsp_comm_s* lsp_comm_t;
+/* Rank 0 creates the id and ships its LSP_COMM_ID_BYTES bytes to every rank. */
+int lsp_comm_unique_id(void* id_out);
+/* Collective over all ranks (ncclCommInitRank); the device is the caller's
+ * current CUDA device. */
+int lsp_comm_init(const void* id, int nranks, int rank, lsp_comm_t* out);
+int lsp_comm_destroy(lsp_comm_t comm);
+int lsp_comm_size(lsp_comm_t comm, int* nranks, int* rank);
+int lsp_nccl_version(int* version);
+/* In-place mean over ranks of count elements (ncclAllReduce, ncclAvg) on stream. */
+int lsp_allreduce_mean(lsp_comm_t comm, void* buf, int64_t count, lsp_dtype dtype,
+                       lsp_stream_t stream);
+/* The layer's whole S^T buffer (lsp_layer_s_buffer) averaged over ranks on
+ * `stream`, then re-checked for non-finite values so that every rank latches
+ * the layer's flag together (call between lsp_layer_compress and
+ * lsp_layer_update/_adam; enqueue on the compress stream or join with events). */
+int lsp_layer_allreduce(lsp_layer_t layer, lsp_comm_t comm, lsp_stream_t stream);
 
 /* ----------------------------------------------------------------------------
  * Projector fit (proj/src/projector.cpp:189-315), on the device in fp64.

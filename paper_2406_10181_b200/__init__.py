@@ -18,6 +18,7 @@ from ._lib import (  # noqa: F401
     InvalidArgument,
     IoError,
     LspError,
+    NcclError,
     NumericError,
     Layout,
     lib,
@@ -27,6 +28,7 @@ from ._lib import (  # noqa: F401
 )
 from .projector import (  # noqa: F401
     AdamState,
+    Comm,
     DevicePair,
     DeviceProjector,
     FitConfig,
@@ -36,6 +38,7 @@ from .projector import (  # noqa: F401
     identity_pattern,
     init_sparse,
     load_projector,
+    nccl_version,
     projector_gram,
     maybe_update,
     reproject_state,
@@ -46,7 +49,7 @@ from .projector import (  # noqa: F401
 )
 
 __all__ = [
-    "AdamState", "DevicePair", "Layer", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
+    "AdamState", "Comm", "nccl_version", "NcclError", "DevicePair", "Layer", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
     "identity_pattern", "init_sparse", "load_projector", "projector_gram", "reproject_state", "maybe_update",
     "save_projector", "step", "subsample_size", "update", "LspError", "InvalidArgument",
     "NumericError", "IoError", "CudaError", "Layout", "lib", "library_path", "launch_count", "set_sm_budget",

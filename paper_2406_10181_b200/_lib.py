@@ -39,7 +39,14 @@ class CudaError(LspError):
     code = 4
 
 
-_ERRORS = {1: InvalidArgument, 2: NumericError, 3: IoError, 4: CudaError, 5: CudaError}
+class NcclError(LspError):
+    """NCCL missing or failed (LSP_ENCCL)."""
+
+    code = 6
+
+
+_ERRORS = {1: InvalidArgument, 2: NumericError, 3: IoError, 4: CudaError, 5: CudaError,
+           6: NcclError}
 
 
 class DType(enum.IntEnum):
@@ -128,6 +135,13 @@ _SIGS = {
     "lsp_fit": (_i, [_vp, C.POINTER(_vp), _i, _i64, _i, C.POINTER(FitConfigC),
                      C.POINTER(FitReportC), _dp, _i, _vp]),
     "lsp_projector_gram": (_i, [_vp, _vp, _vp, _vp]),
+    "lsp_comm_unique_id": (_i, [_vp]),
+    "lsp_comm_init": (_i, [_vp, _i, _i, C.POINTER(_vp)]),
+    "lsp_comm_destroy": (_i, [_vp]),
+    "lsp_comm_size": (_i, [_vp, _ip, _ip]),
+    "lsp_nccl_version": (_i, [_ip]),
+    "lsp_allreduce_mean": (_i, [_vp, _vp, _i64, _i, _vp]),
+    "lsp_layer_allreduce": (_i, [_vp, _vp, _vp]),
     "lsp_reproject_state": (_i, [_vp, _vp, _vp, _i, _vp]),
 }
 

@@ -142,6 +142,15 @@ void layer_update(lsp_layer_s& L, double lr, bool check, cudaStream_t st) {
 
 }  // namespace
 
+namespace lspb {
+void layer_s_view(lsp_layer_s* L, void** buf, long long* count, lsp_dtype* dt, int** flag) {
+  *buf = L->s_t.p;
+  *count = static_cast<long long>(L->count * L->dd());
+  *dt = L->compute;
+  *flag = L->adam.flag.as<int>();
+}
+}  // namespace lspb
+
 extern "C" {
 
 int lsp_layer_create(int count, const lsp_pair_t* pairs, double beta1, double beta2, double eps,

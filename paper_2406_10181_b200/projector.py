@@ -446,6 +446,12 @@ class Layer:
                        ldw, int(_dtype_of(w)))
         self._bound[idx] = (g, w)  # keep the tensors alive
 
+    def allreduce(self, comm, stream=None):
+        """Mean of the layer's S^T buffer over the ranks of ``comm`` (NCCL, on
+        ``stream``), then a finiteness re-check so every rank latches the flag
+        together (lsp_layer_allreduce)."""
+        lib.layer_allreduce(self._h, comm.handle, _stream(stream))
+
     def s_buffer(self):
         """torch view of the layer's S^T buffer [count, d, d] (device memory owned by the layer)."""
         if self._s_view is None:
@@ -586,3 +592,67 @@ def reproject_state(adam: AdamState, old_pair: DevicePair, new_pair: DevicePair,
     """In-place moment transfer into a refitted subspace (subspace_opt.cpp:72-101)."""
     lib.reproject_state(adam.handle, old_pair.handle, new_pair.handle, int(kind),
                         _stream(stream))
+
+
+class Comm:
+    """The library's NCCL communicator (include/lsp_b200.h lsp_comm_*): the data
+    plane of the data-parallel step (SURVEY 8(b) ``lsp_allreduce_S``).  The
+    ncclUniqueId is created by rank 0 and shipped over a torch.distributed
+    group (any backend: gloo is enough for the bootstrap)."""
+
+    ID_BYTES = 128
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes):
+        if len(unique_id) != self.ID_BYTES:
+            raise InvalidArgument("comm: unique id must be 128 bytes")
+        buf = C.create_string_buffer(unique_id, self.ID_BYTES)
+        h = C.c_void_p()
+        lib.comm_init(buf, int(nranks), int(rank), C.byref(h))
+        self._h = h
+        self.nranks, self.rank = int(nranks), int(rank)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(Comm.ID_BYTES)
+        lib.comm_unique_id(buf)
+        return buf.raw
+
+    @classmethod
+    def from_group(cls, group=None):
+        """Collective over ``group`` (torch.distributed): rank 0's id to everyone."""
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        return cls(world, rank, obj[0])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def allreduce_mean(self, t, stream=None):
+        """In-place mean over ranks of a contiguous CUDA tensor (f64 / f32 / bf16)."""
+        if not t.is_cuda or not t.is_contiguous():
+            raise InvalidArgument("allreduce_mean: expected a contiguous CUDA tensor")
+        lib.allreduce_mean(self._h, C.c_void_p(t.data_ptr()), t.numel(), int(_dtype_of(t)),
+                           _stream(stream))
+        return t
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_version() -> int:
+    v = C.c_int()
+    lib.nccl_version(C.byref(v))
+    return int(v.value)

@@ -3,24 +3,29 @@
 The reference runs its per-layer loop only after the whole backward pass
 (proj/src/trainer.cpp:186-198) and *models* the paper's layer-wise pipeline in a
 simulator (build_lsp_layerwise, proj/src/schedule_sim.cpp:255-283: per layer
-bwd -> offload -> update -> upload -> apply, deeper layers first).  On B200 the
-offload/upload legs become an NCCL all-reduce of the layer's S over NVLink, and
-the pipeline is real:
+bwd -> offload -> update -> upload -> apply, deeper layers first, and the next
+forward of layer l waits on apply(l), :266).  On B200 the offload/upload legs
+become an NCCL all-reduce of the layer's S over NVLink, and the pipeline is real:
 
     for layer l in backward order (last layer first):
-        compress(l)                          # S_l = P^T G_l Q, one grouped launch
-        all_reduce(S_l, mean)  async         # rides on NCCL's stream
-        finish(l+1): wait(S_{l+1}) -> Adam -> W -= lr P dS Q^T
+        [bwd(l) on the compute stream -> G_l]            (backward=...)
+        compress(l)            S_l = P^T G_l Q, one grouped launch (waits on G_l)
+        all_reduce(S_l, mean)  on the comm stream                 (world > 1)
+        finish(l+1): wait(S_{l+1}) -> Adam -> Y build -> W -= lr P dS Q^T
 
 so the all-reduce of layer l overlaps the compress of layer l-1 and the apply of
-layer l+1.  With ``streams=(compress_stream, update_stream)`` (concurrent mode)
-the compress chain and the update chain (Adam -> Y build -> W stream) also run
-on two CUDA streams, joined by one event per layer: the compress of layer l-1
-(an L2-gather-latency-bound kernel) overlaps the HBM-bound W update of layer
-l+1 on the device.  ``lsp_set_sm_budget`` sizes the two persistent grids so
-neither starves the other.  Anything that exposes ``compress()``, ``s_buffer()``, ``adam(check)``
-and ``apply(lr)`` can be scheduled: ``paper_2406_10181_b200.Layer`` on the GPU,
-or a CPU stand-in (tests/test_dist_cpu.py runs this exact class over gloo).
+layer l+1, and -- with a ``backward`` producer -- the compress of layer l (an
+L2-latency-bound kernel) runs on a side stream while the compute stream already
+executes the backward GEMMs of layer l-1.  The next step's work on the compute
+stream waits on every apply (the forward of layer l needs W_l updated).
+
+Data plane: ``comm`` (paper_2406_10181_b200.Comm, the library's own NCCL
+communicator, lsp_layer_allreduce) or ``group`` (torch.distributed: NCCL AVG,
+or gloo sum-then-scale for the CPU stand-in tests).
+
+Anything that exposes ``compress()``, ``s_buffer()``, ``adam(check)`` and
+``apply(lr)`` can be scheduled: ``paper_2406_10181_b200.Layer`` on the GPU, or a
+CPU stand-in (tests/test_dist_cpu.py runs this exact class over gloo).
 """
 from __future__ import annotations
 
@@ -29,18 +34,34 @@ from typing import Callable, Optional, Sequence
 
 class LayerSchedule:
     def __init__(self, layers: Sequence, lr: float, group=None,
-                 record: Optional[Callable[[str, int, str], None]] = None, streams=None):
-        """layers: in forward order; group: a torch.distributed process group or
-        None for a single rank; record(phase, layer, "begin"|"end") is called
-        around every stage (bench.py hangs CUDA events on it)."""
+                 record: Optional[Callable[[str, int, str], None]] = None, streams=None,
+                 comm=None, backward: Optional[Callable[[int], None]] = None,
+                 lsp_stream=None, comm_stream=None):
+        """layers: in forward order.
+        group: a torch.distributed process group or None (single rank).
+        comm: a paper_2406_10181_b200.Comm (the library's NCCL communicator);
+            takes precedence over ``group`` for the S all-reduce.
+        record(phase, layer, "begin"|"end"): called around every stage on the
+            stream the stage runs on (bench.py hangs CUDA events on it).
+        streams: None or (compress stream, update stream) -- concurrent mode.
+        backward(li): enqueue the backward of layer li (producing its bound
+            gradients) on the current (compute) stream; the LSP chain then runs
+            on ``lsp_stream`` gated by one event per layer.
+        """
         self.layers = list(layers)
         self.lr = lr
         self.group = group
+        self.comm = comm
         self.record = record
-        self.streams = streams  # None or (compress stream, update stream), torch.cuda.Stream
+        self.streams = streams
+        self.backward = backward
+        self.lsp_stream = lsp_stream
+        self.comm_stream = comm_stream
         self._events = None
         self.world = 1
-        if group is not None:
+        if comm is not None:
+            self.world = comm.nranks
+        elif group is not None:
             import torch.distributed as dist
 
             self.world = dist.get_world_size(group)
@@ -49,7 +70,10 @@ class LayerSchedule:
         if self.record is not None:
             self.record(phase, li, when)
 
+    # ---- the all-reduce of one layer's S ---------------------------------
     def _allreduce(self, li):
+        if self.comm is not None:  # also at nranks == 1 (an identity exchange)
+            return self._allreduce_comm(li)
         if self.world == 1:
             return None
         import torch.distributed as dist
@@ -61,6 +85,34 @@ class LayerSchedule:
         return _SumThenScale(dist.all_reduce(buf, group=self.group, async_op=True), buf,
                              1.0 / self.world)
 
+    def _allreduce_comm(self, li):
+        """lsp_layer_allreduce on the comm stream, ordered after compress(li)."""
+        import torch
+
+        ev = self._ev()
+        src = torch.cuda.current_stream()
+        cs = self.comm_stream
+        if cs is None:
+            cs = self.comm_stream = torch.cuda.Stream()
+        ev["compressed"][li].record(src)
+        with torch.cuda.stream(cs):
+            cs.wait_event(ev["compressed"][li])
+            self._rec("allreduce", li, "begin")
+            self.layers[li].allreduce(self.comm)
+            self._rec("allreduce", li, "end")
+            ev["reduced"][li].record(cs)
+        return _EventWork(ev["reduced"][li])
+
+    def _ev(self):
+        import torch
+
+        if self._events is None:
+            n = len(self.layers)
+            self._events = {k: [torch.cuda.Event() for _ in range(n)]
+                            for k in ("compressed", "reduced", "grad", "update")}
+        return self._events
+
+    # ---- Adam + apply of one layer ---------------------------------------
     def _finish(self, li, work):
         if work is not None:
             work.wait()
@@ -84,6 +136,8 @@ class LayerSchedule:
         return list(reversed(range(len(self.layers))))
 
     def step(self):
+        if self.backward is not None:
+            return self._step_backward()
         if self.streams is not None:
             return self._step_concurrent()
         pending = None
@@ -98,13 +152,44 @@ class LayerSchedule:
         if pending is not None:
             self._finish(*pending)
 
+    def _step_backward(self):
+        """Backward producer on the compute (current) stream; compress, Adam and
+        apply on the LSP stream, each compress(l) gated by the event that
+        follows bwd(l); the all-reduce on the comm stream.  The compute stream
+        waits on the LSP stream at the end (the next forward needs W)."""
+        import torch
+
+        main = torch.cuda.current_stream()
+        ls = self.lsp_stream
+        if ls is None:
+            ls = self.lsp_stream = torch.cuda.Stream()
+        ev = self._ev()
+        ls.wait_stream(main)  # previous work on the compute stream (e.g. the forward)
+        pending = None
+        for li in self.order():
+            self._rec("backward", li, "begin")
+            self.backward(li)
+            self._rec("backward", li, "end")
+            ev["grad"][li].record(main)
+            with torch.cuda.stream(ls):
+                ls.wait_event(ev["grad"][li])
+                self._rec("compress", li, "begin")
+                self.layers[li].compress()
+                self._rec("compress", li, "end")
+                work = self._allreduce(li)
+                if pending is not None:
+                    self._finish(*pending)
+                pending = (li, work)
+        with torch.cuda.stream(ls):
+            if pending is not None:
+                self._finish(*pending)
+        main.wait_stream(ls)
 
     def _step_concurrent(self):
         import torch
 
         sc, su = self.streams
-        if self._events is None:
-            self._events = [torch.cuda.Event() for _ in self.layers]
+        ev = self._ev()
         main = torch.cuda.current_stream()
         sc.wait_stream(main)
         su.wait_stream(main)
@@ -115,24 +200,24 @@ class LayerSchedule:
                 self.layers[li].compress()
                 self._rec("compress", li, "end")
                 work = self._allreduce(li)
-                ev = None
+                e = None
                 if work is None:
-                    ev = self._events[li]
-                    ev.record(sc)
+                    e = ev["compressed"][li]
+                    e.record(sc)
             if pending is not None:
                 self._finish_on(su, *pending)
-            pending = (li, work, ev)
+            pending = (li, work, e)
         if pending is not None:
             self._finish_on(su, *pending)
         main.wait_stream(sc)
         main.wait_stream(su)
 
-    def _finish_on(self, su, li, work, ev):
+    def _finish_on(self, su, li, work, e):
         import torch
 
         with torch.cuda.stream(su):
-            if ev is not None:
-                su.wait_event(ev)
+            if e is not None:
+                su.wait_event(e)
             self._finish(li, work)
 
 
@@ -143,3 +228,16 @@ class _SumThenScale:
     def wait(self):
         self.work.wait()
         self.buf.mul_(self.scale)
+
+
+class _EventWork:
+    """Completion of an all-reduce enqueued on the comm stream: the consumer's
+    current stream waits on its event (no host blocking)."""
+
+    def __init__(self, event):
+        self.event = event
+
+    def wait(self):
+        import torch
+
+        torch.cuda.current_stream().wait_event(self.event)

@@ -1,0 +1,170 @@
+"""GPU: the library's NCCL data plane (lsp_comm_*, lsp_layer_allreduce) and the
+backward-overlapped layer schedule (north-star subsystem 5).
+
+Only one GPU is available per call, so the NCCL communicator runs with one
+rank (NCCL refuses two ranks on one device); the multi-rank semantics are the
+gloo tests' (tests/test_dist_cpu.py, tests/test_gpu_dp.py).  Bitwise checks:
+the schedule with the comm-stream all-reduce and the schedule with a backward
+producer on the compute stream (compress on a side stream, gated per layer)
+give exactly the weights of the serial schedule.
+"""
+import pytest
+import torch
+
+import paper_2406_10181_b200 as lsp
+from paper_2406_10181_b200.schedule import LayerSchedule
+
+pytestmark = pytest.mark.gpu
+KINIT = 0x1A171
+SHAPES = [(512, 512), (512, 1376), (1376, 512)]
+D, R, L, T = 128, 4, 4, 256
+
+
+@pytest.fixture(scope="module")
+def comm(cuda):
+    c = lsp.Comm(1, 0, lsp.Comm.unique_id())
+    yield c
+    c.close()
+
+
+def test_nccl_loaded(cuda):
+    assert lsp.nccl_version() >= 21000  # ncclAvg needs NCCL >= 2.10
+
+
+def test_comm_allreduce_identity_one_rank(comm):
+    for dt in (torch.float32, torch.float64, torch.bfloat16):
+        x = torch.randn(4097, device="cuda").to(dt)
+        y = x.clone()
+        comm.allreduce_mean(y)
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+
+
+def test_layer_allreduce_latches_nonfinite(comm):
+    P = lsp.DeviceProjector.random(64, 16, 2, 1)
+    Q = lsp.DeviceProjector.random(96, 16, 2, 2)
+    lay = lsp.Layer([lsp.DevicePair(P, Q)])
+    g = torch.randn(64, 96, device="cuda")
+    w = torch.randn(64, 96, device="cuda")
+    w0 = w.clone()
+    lay.bind(0, g, w)
+    lay.compress()
+    lay.s_buffer()[0, 3, 5] = float("inf")  # as if another rank contributed a non-finite S
+    lay.allreduce(comm)
+    lay.update(1e-3)
+    with pytest.raises(lsp.NumericError):
+        lay.check()
+    assert torch.equal(w, w0)
+
+
+def _build(seed=5):
+    layers, ws, acts = [], [], []
+    k = 0
+    gen = torch.Generator(device="cuda")
+    for _ in range(L):
+        pairs, bound, xs = [], [], []
+        for (m, n) in SHAPES:
+            P = lsp.DeviceProjector.random(m, D, R, lsp.derive_seed(seed, KINIT, 2 * k))
+            Q = lsp.DeviceProjector.random(n, D, R, lsp.derive_seed(seed, KINIT, 2 * k + 1))
+            pairs.append(lsp.DevicePair(P, Q))
+            gen.manual_seed(100 + k)
+            x = torch.randn(T, m, device="cuda", generator=gen)
+            dy = torch.randn(T, n, device="cuda", generator=gen)
+            g = torch.empty(m, n, device="cuda")
+            w = 0.02 * torch.randn(m, n, device="cuda", generator=gen)
+            bound.append((g, w))
+            xs.append((x, dy, g))
+            k += 1
+        lay = lsp.Layer(pairs)
+        for i, (gi, wi) in enumerate(bound):
+            lay.bind(i, gi, wi)
+        layers.append(lay)
+        ws.extend(w for _, w in bound)
+        acts.append(xs)
+    return layers, ws, acts
+
+
+def _backward(acts):
+    def bwd(li):  # stand-in weight-gradient GEMMs: G = X^T dY (fp32)
+        for x, dy, g in acts[li]:
+            torch.matmul(x.t(), dy, out=g)
+    return bwd
+
+
+def test_schedule_comm_stream_bitwise(comm):
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    for li in range(L):
+        _backward(aa)(li)
+        _backward(ab)(li)
+    sa = LayerSchedule(la, 1e-3)
+    sb = LayerSchedule(lb, 1e-3, comm=comm)
+    for _ in range(3):
+        sa.step()
+        sb.step()
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_backward_overlap_bitwise(cuda, comm, with_comm):
+    """Backward producer on the compute stream, compress(l) on the LSP stream
+    gated by bwd(l)'s event, Adam/apply pipelined one layer behind: weights
+    bitwise equal to 'whole backward, then the serial schedule'."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    sa = LayerSchedule(la, 1e-3)
+    sb = LayerSchedule(lb, 1e-3, backward=_backward(ab), comm=comm if with_comm else None)
+    seen = []
+    sb.record = lambda ph, li, when: seen.append((ph, li, when))
+    for _ in range(2):
+        for li in reversed(range(L)):
+            _backward(aa)(li)
+        sa.step()
+        sb.step()
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+    # backward order, compress(l) issued right after bwd(l)
+    assert seen[0] == ("backward", L - 1, "begin")
+    assert seen[2] == ("compress", L - 1, "begin")
+
+
+def test_backward_overlap_graph_capture(cuda):
+    """The pipelined step (two streams, per-layer events) captures into one CUDA
+    graph; replays match eager steps bitwise."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    la, wa, aa = _build()
+    sa = LayerSchedule(la, 1e-3, backward=_backward(aa))
+    for _ in range(4):
+        sa.step()
+    lb, wb, ab = _build()
+    sb = LayerSchedule(lb, 1e-3, backward=_backward(ab))
+    sb.step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sb.step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+
+
+def test_c_dp_example_runs(cuda, tmp_path):
+    """examples/dp_layer_step.c: compress -> lsp_layer_allreduce -> update through
+    the C-ABI only, one rank (the multi-rank launch is one process per GPU)."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "examples", "dp_layer_step")
+    if not os.path.exists(exe):
+        pytest.skip("examples/dp_layer_step not built")
+    out = subprocess.run([exe, "0", "1", str(tmp_path / "id.bin"), "3"], capture_output=True,
+                         text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "rank 0/1 steps 3 checksum" in out.stdout
