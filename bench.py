@@ -81,14 +81,28 @@ def parse():
                     help="1: compress and update chains on two streams (schedule.py)")
     ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
     ap.add_argument("--sms-update", type=int, default=0, help="lsp_set_sm_budget update SMs")
+    ap.add_argument("--overlap-bwd", type=int, default=0, metavar="TOKENS",
+                    help="backward-overlap mode: stand-in weight-gradient GEMMs G = X^T dY "
+                         "(TOKENS rows) on the compute stream produce every G, the LSP chain "
+                         "runs on a side stream gated per layer (schedule.py); reports the "
+                         "exposed LSP time vs backward alone (0: off)")
+    ap.add_argument("--timeline-out", default=None,
+                    help="with --overlap-bwd: write the per-stream phase timeline of one step")
+    ap.add_argument("--fit-every", type=int, default=None,
+                    help="projector refresh cadence (trainer check_freq); default 100 for c3 "
+                         "(BASELINE configs[2]), 0 elsewhere: times maybe_update per shape")
+    ap.add_argument("--fit-ring", type=int, default=8,
+                    help="extra ring gradients passed to the fit (trainer ring_capacity)")
+    ap.add_argument("--c5-layers", type=int, default=4,
+                    help="c5: independent 4096 x 11008 matrices per step (inputs > L2)")
     return ap.parse_args()
 
 
 def workload(args):
     if args.config == "c5":
         d, r = args.d or 1024, args.r or 4
-        return (f"4096x11008 d/r sweep, d={d}, r={r}, fp32 (BASELINE configs[4])", 1,
-                [(4096, 11008, 1)], d, r, "f32", "f32")
+        return (f"4096x11008 d/r sweep, d={d}, r={r}, fp32 (BASELINE configs[4])",
+                args.c5_layers, [(4096, 11008, 1)], d, r, "f32", "f32")
     desc, L, shapes, d, r, gdt, wdt = CONFIGS[args.config]
     if args.d:
         d = args.d
@@ -172,12 +186,31 @@ class Clocks:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+KERNEL_SOURCES = ("apply.cu", "compress.cu", "compress_spmm.cu", "elementwise.cu", "layer.cu",
+                  "core.cuh", "tma.cuh")
+
+
+def kernel_source_hash():
+    """sha256 over the step kernels' sources: a committed ncu capture is current
+    only if it was taken with the same sources (profiles/<tag>_srchash.txt)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        p = os.path.join(ROOT, "paper_2406_10181_b200", "csrc", f)
+        if os.path.exists(p):
+            h.update(open(p, "rb").read())
+    return h.hexdigest()
+
+
 def profiled_traffic(kernel_prefix, config):
     """DRAM bytes (read + write) of one launch of the roofline kernel from the
     committed ncu --set full summary (profiles/<round>_kernels.md, captured with
-    this bench's own C4 command); None for other configs or when absent."""
+    this bench's own C4 command); None for other configs or when absent.
+    Returns (bytes, source, stale): stale when the capture's source hash
+    (profiles/<tag>_srchash.txt) differs from the current kernel sources."""
     if config != "c4":
-        return None, None
+        return None, None, None
     import glob
     import re
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.md")))
@@ -194,8 +227,11 @@ def profiled_traffic(kernel_prefix, config):
                 if m:
                     vals[key] = float(m.group(1)) * units.get(m.group(2), 1)
             if len(vals) == 2:
-                return vals["dram read"] + vals["dram write"], os.path.relpath(path, ROOT)
-    return None, None
+                hp = path.replace("_kernels.md", "_srchash.txt")
+                cap = open(hp).read().strip() if os.path.exists(hp) else None
+                return (vals["dram read"] + vals["dram write"], os.path.relpath(path, ROOT),
+                        cap != kernel_source_hash())
+    return None, None, None
 
 
 def measured_peaks():
@@ -210,12 +246,39 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference (oracle/_ref) or the oracle port, on host cores
 # ---------------------------------------------------------------------------
-def cpu_baseline(desc, L, shapes, d, r, gdt, lr, reps=1, target_s=12.0):
+def cpu_info():
+    """nproc and the CPU model (lscpu, else /proc/cpuinfo)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    if model is None:
+        try:
+            for line in open("/proc/cpuinfo"):
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        except OSError:
+            pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def cpu_baseline(desc, L, shapes, d, r, gdt, lr, reps=1, single=True):
+    """The reference's own step (oracle/_ref: compress, adam_step, W -= decompress*lr)
+    timed on the host cores in two modes (SURVEY 8(d)): all cores (std::threads
+    over independent matrices, a bounded sample of layers) -> "value"; and one
+    thread, one matrix of each layer shape, serial -> "single_thread"."""
     import oracle
 
     kind = "reference" if oracle.available("reference") else "port"
     O = oracle.Oracle(kind)
-    cores = os.cpu_count() or 1
+    info = cpu_info()
+    cores = info["nproc"]
     per_layer = sum(c for _, _, c in shapes)
     layers = max(1, cores // per_layer)
     rng = np.random.default_rng(0)
@@ -226,8 +289,6 @@ def cpu_baseline(desc, L, shapes, d, r, gdt, lr, reps=1, target_s=12.0):
         g = rng.standard_normal((m, n)).astype(np.float32).astype(np.float64)
         w = (0.02 * rng.standard_normal((m, n))).astype(np.float32).astype(np.float64)
         jobs.append((P, Q, g, w, cnt * layers))
-    threads = sum(j[4] for j in jobs)
-    times = []
     if kind != "reference":
         # the port has no threaded timer: time one matrix per shape serially
         t0 = time.perf_counter()
@@ -238,8 +299,10 @@ def cpu_baseline(desc, L, shapes, d, r, gdt, lr, reps=1, target_s=12.0):
             O.decompress_apply(P, Q, de, lr, w)
         t = time.perf_counter() - t0
         gb = sum(P.n_rows * Q.n_rows for P, Q, *_ in jobs) * BYTES[gdt] / 1e9
-        return {"value": gb / t, "unit": "GB/s", "cores": 1, "kind": kind,
+        return {"value": gb / t, "unit": "GB/s", "cores": 1, "kind": kind, **info,
                 "sample": f"one matrix of each layer shape, serial, {t:.1f}s"}, t
+    threads = sum(j[4] for j in jobs)
+    times = []
     for _ in range(reps):
         res = [0.0] * len(jobs)
 
@@ -256,11 +319,20 @@ def cpu_baseline(desc, L, shapes, d, r, gdt, lr, reps=1, target_s=12.0):
         times.append(time.perf_counter() - t0)
     t = float(np.median(times))
     gb = layers * sum(m * n * c for m, n, c in shapes) * BYTES[gdt] / 1e9
-    return {"value": gb / t, "unit": "GB/s", "cores": threads, "kind": kind,
-            "sample": (f"{layers} layer(s) = {threads} matrices of the {desc.split(',')[0]} "
-                       f"shapes, one reference step each (compress, adam_step, "
-                       f"W -= decompress*lr) on {threads} std::threads, median of {reps}; "
-                       f"{t:.1f}s per sample")}, t
+    out = {"value": gb / t, "unit": "GB/s", "cores": threads, "kind": kind, **info,
+           "sample": (f"{layers} layer(s) = {threads} matrices of the {desc.split(',')[0]} "
+                      f"shapes, one reference step each (compress, adam_step, "
+                      f"W -= decompress*lr) on {threads} std::threads, median of {reps}; "
+                      f"{t:.1f}s per sample")}
+    if single:
+        ts = [O.time_step(P, Q, g, w, lr, 1, 1) for P, Q, g, w, _ in jobs]
+        gb1 = sum(P.n_rows * Q.n_rows for P, Q, *_ in jobs) * BYTES[gdt] / 1e9
+        out["single_thread"] = {
+            "value": gb1 / sum(ts), "unit": "GB/s", "cores": 1,
+            "sample": ("one matrix of each layer shape (" +
+                       ", ".join(f"{P.n_rows}x{Q.n_rows}: {x:.2f}s" for (P, Q, *_), x in
+                                 zip(jobs, ts)) + "), one reference step each, 1 thread")}
+    return out, t
 
 
 def run_reference(args):
@@ -269,8 +341,9 @@ def run_reference(args):
     if rank != 0:
         return
     samples = []
-    for _ in range(args.warmup + args.steps):
-        cb, t = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr)
+    nrun = args.warmup + args.steps
+    for i in range(nrun):
+        cb, t = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr, single=(i == nrun - 1))
         samples.append(cb)
     vals = [c["value"] for c in samples[args.warmup:]]
     v = float(np.median(vals))
@@ -351,8 +424,11 @@ def run_ours(args):
     streams = None
     if args.concurrent:
         streams = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
-    sched = LayerSchedule(layers, args.lr, group=dist.group.WORLD if world > 1 else None,
-                          record=record, streams=streams)
+    # N > 1: the library's own NCCL communicator carries the S all-reduce
+    # (lsp_layer_allreduce on a comm stream; torch.distributed only bootstraps
+    # the id and runs the barriers / max-over-ranks timing)
+    comm = lsp.Comm.from_group() if world > 1 else None
+    sched = LayerSchedule(layers, args.lr, comm=comm, record=record, streams=streams)
 
     def one_step(record=False):
         recording[0] = record
@@ -363,7 +439,7 @@ def run_ours(args):
         one_step()
     torch.cuda.synchronize()
     graph, graph_launches = None, 0
-    if args.graph and world == 1:
+    if args.graph:  # the NCCL all-reduce on the comm stream is captured too (N > 1)
         one_step(record=True)  # per-phase split (eager), outside the timed region
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
@@ -423,7 +499,7 @@ def run_ours(args):
     app_avg = float(np.mean(app_ms))
     comp_avg = float(np.mean(comp_ms))
     app_ach = app_bytes / (app_avg * 1e-3) / 1e9
-    traffic, traffic_src = profiled_traffic("k_apply_y<float", args.config)
+    traffic, traffic_src, traffic_stale = profiled_traffic("k_apply_y<float", args.config)
     comp_ach = comp_bytes / (comp_avg * 1e-3) / 1e9
     tsum = sum(app_ms) + sum(comp_ms) + sum(adam_ms) + sum(build_ms)
     line = {
@@ -455,6 +531,7 @@ def run_ours(args):
                      "traffic_source": (f"{traffic_src}: ncu --set full dram__bytes_read.sum + "
                                         "dram__bytes_write.sum of one launch (includes the "
                                         "Y-block reads from HBM)") if traffic else None,
+                     "traffic_stale": traffic_stale,
                      "peak_source": peak_src,
                      "bytes_per_launch_avg": app_bytes, "avg_launch_ms": app_avg,
                      "share_of_step": sum(app_ms) / (ms if ms > 0 else 1)},
@@ -481,18 +558,165 @@ def run_ours(args):
                                  "profile": args.profile_out,
                                  "transition_layer": cal.transition_layer(prof),
                                  **{k: v for k, v in est.items()}}
+    if args.overlap_bwd > 0:
+        line["overlap"] = overlap_bwd(args, items, layers, L, lsp, torch, dev, comm, gdt)
+    fit_every = args.fit_every if args.fit_every is not None else (
+        100 if args.config == "c3" else 0)
+    if fit_every > 0 and rank == 0:
+        args.fit_every = fit_every
+        line["fit"] = fit_leg(args, items, L, shapes, d, r, lsp, torch, dev)
+        line["fit"]["ms_per_step_incl_fit"] = ms + line["fit"]["amortized_ms_per_step"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, _ = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr)
         line["cpu_baseline"] = cb
     if not args.no_e2e:
-        line["e2e"] = e2e(args, items, layers, order, world, dist, torch, dev, bg)
+        line["e2e"] = e2e(args, items, layers, order, world, dist, torch, dev, bg, comm)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def e2e(args, items, layers, order, world, dist, torch, dev, bg):
+def overlap_bwd(args, items, layers, L, lsp, torch, dev, comm, gdt):
+    """North-star subsystem 5 measured: stand-in weight-gradient GEMMs
+    (G = X^T dY with args.overlap_bwd token rows; TF32 for fp32 G, bf16 for bf16
+    G) produce every layer's gradients on the compute stream, last layer first;
+    the LSP chain (compress -> [all-reduce] -> Adam -> Y -> apply) runs on a side
+    stream, compress(l) gated by bwd(l)'s event (schedule.py).  Times, per step,
+    CUDA-graph replays of (a) the backward alone, (b) backward then the serial
+    LSP step, (c) the pipelined step; exposed LSP = (c) - (a)."""
+    from paper_2406_10181_b200.schedule import LayerSchedule
+
+    T = args.overlap_bwd
+    torch.backends.cuda.matmul.allow_tf32 = True
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[gdt]
+    per_layer = len(items) // L
+    acts = {}
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(17)
+    for it in items:
+        for dim in (it["m"], it["n"]):
+            if dim not in acts:
+                acts[dim] = torch.randn(T, dim, device=dev, generator=gen).to(tdt)
+
+    def backward(li):
+        for it in items[li * per_layer:(li + 1) * per_layer]:
+            torch.matmul(acts[it["m"]].t(), acts[it["n"]], out=it["g"])
+
+    order = list(reversed(range(L)))
+    serial = LayerSchedule(layers, args.lr, comm=comm)
+    piped = LayerSchedule(layers, args.lr, comm=comm, backward=backward)
+
+    def bwd_all():
+        for li in order:
+            backward(li)
+
+    def bwd_then_lsp():
+        bwd_all()
+        serial.step()
+
+    variants = {"bwd_only": bwd_all, "bwd_then_lsp": bwd_then_lsp, "pipelined": piped.step}
+    graphs = {}
+    for name, fn in variants.items():
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        graphs[name] = g
+    res = {}
+    stream = torch.cuda.current_stream()
+    for name, g in graphs.items():
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        res[name] = t0.elapsed_time(t1) / args.steps
+    lsp_serial = res["bwd_then_lsp"] - res["bwd_only"]
+    exposed = res["pipelined"] - res["bwd_only"]
+    out = {"tokens": T, "gemm": "tf32" if gdt == "f32" else "bf16",
+           "bwd_only_ms": res["bwd_only"], "bwd_then_lsp_ms": res["bwd_then_lsp"],
+           "pipelined_ms": res["pipelined"], "lsp_serial_ms": lsp_serial,
+           "exposed_lsp_ms": exposed,
+           "hidden_frac": (1.0 - exposed / lsp_serial) if lsp_serial > 0 else None,
+           "note": "CUDA-graph replays; exposed = pipelined - backward alone"}
+    if args.timeline_out:
+        out["timeline"] = args.timeline_out
+        write_timeline(args.timeline_out, piped, torch, T)
+    return out
+
+
+def write_timeline(path, sched, torch, T):
+    """One eager pipelined step with CUDA events around every stage on the stream
+    it runs on: per-stream start/end times (ms from the step start) as JSON."""
+    evs = []
+    start = torch.cuda.Event(enable_timing=True)
+
+    def rec(ph, li, when):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream())
+        evs.append((ph, li, when, e, torch.cuda.current_stream().stream_id))
+
+    sched.record = rec
+    torch.cuda.synchronize()
+    start.record(torch.cuda.current_stream())
+    sched.step()
+    torch.cuda.synchronize()
+    sched.record = None
+    spans = {}
+    for ph, li, when, e, sid in evs:
+        spans.setdefault((ph, li, sid), {})[when] = start.elapsed_time(e)
+    rows = [{"phase": ph, "layer": li, "stream": sid, "begin_ms": v.get("begin"),
+             "end_ms": v.get("end")} for (ph, li, sid), v in spans.items()]
+    rows.sort(key=lambda x: x["begin_ms"])
+    with open(path, "w") as f:
+        json.dump({"tokens": T, "spans": rows}, f, indent=1)
+
+
+def fit_leg(args, items, L, shapes, d, r, lsp, torch, dev):
+    """BASELINE configs[2]'s "projector fit every 100 steps": one maybe_update
+    (trainer.cpp:74-112: relative-bias gate at alpha 0.5, fresh pair, fit on
+    the gradient plus args.fit_ring ring gradients with the reference FitConfig
+    defaults -- <= 500 GD steps with line search --, reproject the moments) per
+    distinct matrix shape, timed on the device; amortised over the cadence."""
+    every = args.fit_every
+    per = []
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(23)
+    seen = set()
+    for it in items:
+        key = (it["m"], it["n"])
+        if key in seen:
+            continue
+        seen.add(key)
+        cnt = sum(c for (m, n, c) in shapes if (m, n) == key) * L
+        ring = [torch.randn(it["m"], it["n"], device=dev, generator=gen).to(it["g"].dtype)
+                for _ in range(args.fit_ring)]
+        adam = lsp.AdamState(d)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        newp, res = lsp.maybe_update(it["pair"], adam, it["g"], ring, r=r, alpha=0.5,
+                                     fit=lsp.FitConfig(), reinit_seed=len(per) + 1)
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t0) * 1e3
+        per.append({"shape": list(key), "matrices": cnt, "maybe_update_ms": ms,
+                    "refreshed": bool(res["refreshed"]), "fit_steps": int(res["fit_steps"]),
+                    "fit_timed_out": bool(res["fit_timed_out"]),
+                    "bias_before": res["bias_before"], "bias_after": res["bias_after"]})
+        del ring
+    per_check = sum(x["maybe_update_ms"] * x["matrices"] for x in per)
+    return {"every": every, "targets": 1 + args.fit_ring, "per_shape": per,
+            "ms_per_check": per_check, "amortized_ms_per_step": per_check / every,
+            "note": ("fp64 device fit (csrc/fit.cu); one maybe_update per shape timed, "
+                     "times the shape's matrix count; not part of the grad GB/s metric")}
+
+
+def e2e(args, items, layers, order, world, dist, torch, dev, bg, comm=None):
     """Same metric through the C-ABI with HOST gradients: every step copies each
     layer's G matrices from pinned host memory (copy stream, double-buffered per
     layer) into the bound device buffers, runs the layer step, and reads the
@@ -529,9 +753,9 @@ def e2e(args, items, layers, order, world, dist, torch, dev, bg):
             main.wait_event(e)
             lay = layers[li]
             lay.compress()
-            if world > 1:
-                dist.all_reduce(lay.s_buffer(), op=dist.ReduceOp.AVG)
-            lay.update(args.lr, check_finite=world > 1)
+            if comm is not None:
+                lay.allreduce(comm)
+            lay.update(args.lr)
             s_host[li].copy_(lay.s_buffer(), non_blocking=True)
         torch.cuda.synchronize()
 

@@ -235,3 +235,41 @@ def test_maybe_update_gate_and_zero_grad(cuda, reference):
     assert np.array_equal(mo, mm) and np.array_equal(vo, vv)
     same, res = lsp.maybe_update(pair, adam, dev(np.zeros((m, n))), [], r=r, alpha=0.1)
     assert same is pair and res["skipped_zero_grad"] and np.isnan(res["bias_before"])
+
+
+def test_fit_loss_gradient_c3_shape_vs_reference(cuda, reference):
+    """BASELINE configs[2] scale: fit_loss and fit_gradient (Eq. 3) on the
+    2048 x 5504 MLP shape, d = 1024, r = 4, one target (T = 1), against the
+    compiled reference (its dense fit_gradient takes ~20 s per target here,
+    SURVEY 7.3(5)).  fp64 device compute, tolerance 1e-10 (loss) / 1e-9
+    (gradient: different association of the same sums)."""
+    m, n, d, r = 2048, 5504, 1024, 4
+    P = reference.init_sparse(m, d, r, reference.derive_seed(1, 0x1A171, 2))
+    Q = reference.init_sparse(n, d, r, reference.derive_seed(1, 0x1A171, 3))
+    g = np.random.default_rng(2048).standard_normal((m, n))
+    cfg = lsp.FitConfig(reg_beta=1e-3)
+    pair = dpair(P, Q)
+    loss = pair.fit_loss([dev(g)], cfg)
+    assert loss == pytest.approx(reference.fit_loss(P, Q, [g], reg_beta=1e-3), rel=1e-10)
+    gp, gq = pair.fit_gradient([dev(g)], cfg)
+    gp_ref, gq_ref = reference.fit_gradient(P, Q, [g], reg_beta=1e-3)
+    assert rel(gp, gp_ref) < 1e-9 and rel(gq, gq_ref) < 1e-9
+
+
+def test_reproject_d1024_vs_oracle(cuda, port):
+    """reproject_state at d = 1024 (the dense d^3 transfer products, k_dgemm) on
+    the C3 MLP projectors, against the oracle, both transfer kinds."""
+    m, n, d, r = 2048, 5504, 1024, 4
+    oP, oQ = port.init_sparse(m, d, r, 1), port.init_sparse(n, d, r, 2)
+    nP, nQ = port.init_sparse(m, d, r, 3), port.init_sparse(n, d, r, 4)
+    rng = np.random.default_rng(1)
+    mm, vv = rng.standard_normal((d, d)) * 1e-3, (rng.standard_normal((d, d)) * 1e-3) ** 2
+    old, new = dpair(oP, oQ), dpair(nP, nQ)
+    for kind in (0, 1):
+        a = lsp.AdamState(d, compute="f64")
+        a.set(mm, vv, 100)
+        lsp.reproject_state(a, old, new, kind)
+        mo, vo, st = a.get()
+        mref, vref = port.reproject_state(oP, oQ, nP, nQ, mm, vv, kind)
+        assert st == 100
+        assert rel(mo, mref) < 1e-12 and rel(vo, vref) < 1e-12
