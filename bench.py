@@ -86,6 +86,12 @@ def parse():
                          "(TOKENS rows) on the compute stream produce every G, the LSP chain "
                          "runs on a side stream gated per layer (schedule.py); reports the "
                          "exposed LSP time vs backward alone (0: off)")
+    ap.add_argument("--bwd-carveout", type=int, default=0,
+                    help="with --overlap-bwd: SMs the backward GEMMs leave free "
+                         "(torch SM carve-out for cuBLAS) and the LSP persistent grids use "
+                         "(lsp_set_sm_budget); 0: no partition")
+    ap.add_argument("--lsp-priority", type=int, default=0,
+                    help="with --overlap-bwd: 1 = the LSP stream gets the higher priority")
     ap.add_argument("--timeline-out", default=None,
                     help="with --overlap-bwd: write the per-stream phase timeline of one step")
     ap.add_argument("--fit-every", type=int, default=None,
@@ -605,7 +611,16 @@ def overlap_bwd(args, items, layers, L, lsp, torch, dev, comm, gdt):
 
     order = list(reversed(range(L)))
     serial = LayerSchedule(layers, args.lr, comm=comm)
-    piped = LayerSchedule(layers, args.lr, comm=comm, backward=backward)
+    lsp_stream = None
+    if args.lsp_priority:
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+            else (0, -1)
+        lsp_stream = torch.cuda.Stream(device=dev, priority=-1)
+    piped = LayerSchedule(layers, args.lr, comm=comm, backward=backward, lsp_stream=lsp_stream)
+    carve = args.bwd_carveout
+    if carve:
+        torch._C._set_sm_carveout_experimental(carve)
+        lsp.set_sm_budget(carve, carve)
 
     def bwd_all():
         for li in order:
@@ -637,9 +652,13 @@ def overlap_bwd(args, items, layers, L, lsp, torch, dev, comm, gdt):
         t1.record(stream)
         torch.cuda.synchronize()
         res[name] = t0.elapsed_time(t1) / args.steps
+    if carve:
+        torch._C._set_sm_carveout_experimental(None)
+        lsp.set_sm_budget(args.sms_compress, args.sms_update)
     lsp_serial = res["bwd_then_lsp"] - res["bwd_only"]
     exposed = res["pipelined"] - res["bwd_only"]
-    out = {"tokens": T, "gemm": "tf32" if gdt == "f32" else "bf16",
+    out = {"tokens": T, "gemm": "tf32" if gdt == "f32" else "bf16", "carveout_sms": carve,
+           "lsp_stream_priority": "high" if args.lsp_priority else "default",
            "bwd_only_ms": res["bwd_only"], "bwd_then_lsp_ms": res["bwd_then_lsp"],
            "pipelined_ms": res["pipelined"], "lsp_serial_ms": lsp_serial,
            "exposed_lsp_ms": exposed,
