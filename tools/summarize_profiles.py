@@ -83,6 +83,17 @@ def full_metrics(rep):
         if key in hdr:
             i = hdr.index(key)
             got[label] = f"{vals[i]} {units[i]}".strip()
+    st = {}
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+            try:
+                st[h[len("smsp__pcsamp_warps_issue_stalled_"):]] = float(vals[i])
+            except ValueError:
+                pass
+    tot = sum(st.values())
+    if tot > 0:
+        top = sorted(st.items(), key=lambda kv: -kv[1])[:4]
+        got["top stalls (pc samples)"] = ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in top)
     return got
 
 
@@ -127,6 +138,11 @@ def main():
             for k, v in m.items():
                 f.write(f"| {k} | {v} |\n")
             f.write("\n")
+    sys.path.insert(0, os.getcwd())
+    import bench  # the same hash bench.py checks roofline.traffic against
+
+    with open(f"profiles/{tag}_srchash.txt", "w") as f:
+        f.write(bench.kernel_source_hash() + "\n")
     print(open(f"profiles/{tag}_launches.md").read())
     print(open(f"profiles/{tag}_kernels.md").read())
 
