@@ -172,7 +172,7 @@ constexpr int kDsMaxD = 1536;
 
 struct Y2Args {
   YMat mat[kMaxGroup];
-  int count, d, ablocks;
+  int count, d, ablocks, tbuf;  // tbuf: transposed write-out (BN == 32, smem permitting)
   long long units;  // mat[i].task_end: cumulative units
   const int* skip;
 };
@@ -295,7 +295,18 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_build_y_smem(const __grid_c
 #pragma unroll
         for (int l = 0; l < KR; ++l) y[jj] = fmaf(en.v[l], ds[en.p[l] * 32 + lane], y[jj]);
       }
-      if (a < d) {
+      if (A.tbuf) {
+        // transposed write-out through a per-warp 32 x 33 buffer: every store
+        // is one 128-byte row segment Yb[band][a0 + rr][0..31]
+        float* tb = ds + d * 32 + kYWarps * 2 * NQ * 4 + warp * 32 * 33;
+        __syncwarp();
+#pragma unroll
+        for (int jj = 0; jj < BN; ++jj) tb[lane * 33 + jj] = y[jj];
+        __syncwarp();
+        float* o = M.yb + (static_cast<long long>(band) * d + a0) * BN;
+        const int rows = min(32, d - a0);
+        for (int rr = 0; rr < rows; ++rr) o[rr * BN + lane] = tb[rr * 33 + lane];
+      } else if (a < d) {
         float4* o = reinterpret_cast<float4*>(M.yb + (static_cast<long long>(band) * d + a) * BN);
 #pragma unroll
         for (int t = 0; t < BN / 4; ++t)
@@ -896,7 +907,10 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
     return;
   }
   if (use_smem) {
-    const int smem = p0.d * 32 * static_cast<int>(sizeof(float)) + kYWarps * 2 * BN * KR * 4;
+    int smem = p0.d * 32 * static_cast<int>(sizeof(float)) + kYWarps * 2 * BN * KR * 4;
+    const int tbytes = kYWarps * 32 * 33 * static_cast<int>(sizeof(float));
+    B.tbuf = BN == 32 && smem + tbytes <= 227 * 1024;
+    if (B.tbuf) smem += tbytes;
     auto kern = k_build_y_smem<BN, KR>;
     LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int grid = static_cast<int>(std::min<long long>(units, sm_budget(kBudgetUpdate)));
