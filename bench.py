@@ -579,6 +579,9 @@ def run_ours(args):
         line["e2e"] = e2e(args, items, layers, order, world, dist, torch, dev, bg, comm)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()  # before the process group and the CUDA context go away
     if world > 1:
         dist.destroy_process_group()
 

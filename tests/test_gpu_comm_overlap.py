@@ -168,3 +168,28 @@ def test_c_dp_example_runs(cuda, tmp_path):
                          text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert "rank 0/1 steps 3 checksum" in out.stdout
+
+
+def test_schedule_comm_graph_capture(comm):
+    """bench.py --gpus N captures the step with the library's NCCL all-reduce on
+    the comm stream in one CUDA graph; at one rank the replays must equal eager
+    steps bitwise (event fork/join of the comm stream inside the capture)."""
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    for li in range(L):
+        _backward(aa)(li)
+        _backward(ab)(li)
+    sa = LayerSchedule(la, 1e-3, comm=comm)
+    for _ in range(4):
+        sa.step()
+    sb = LayerSchedule(lb, 1e-3, comm=comm)
+    sb.step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sb.step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
