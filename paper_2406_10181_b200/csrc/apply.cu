@@ -32,6 +32,10 @@
 #include "core.cuh"
 #include "tma.cuh"
 
+#ifndef LSP_APPLY_TILE_F32
+#define LSP_APPLY_TILE_F32 8192
+#endif
+
 namespace lspb {
 
 namespace {
@@ -43,7 +47,11 @@ constexpr int kNG = 2;                  // consumer groups
 constexpr int kAThreads = (kNC + 2) * 32;
 constexpr int kMaxStages = 16;
 constexpr int kYChunk = 16 * 1024;      // bulk-copy granule for the Y block
-constexpr int kTileBytes = 16384;       // W bytes per ring tile (BN x TR elements)
+// W bytes per ring tile (BN x TR elements): smaller fp32 tiles keep more of the
+// ring in flight while two tiles are being consumed (C4 apply 10.1 ms per step
+// with 8 KB vs 10.4 with 16 KB); bf16 measured faster with 16 KB (6.8 vs 7.2).
+template <typename Tw>
+constexpr int tile_bytes() { return sizeof(Tw) == 4 ? LSP_APPLY_TILE_F32 : 16384; }
 
 
 // A projector row's (or column's) KR entries, read with the widest vectors KR
@@ -603,7 +611,7 @@ __device__ __forceinline__ float lds_w(unsigned addr) {
 // CPL = 1.
 template <typename Tw, int BN, int KR, bool USE_IN, bool PAIR, int CPL>
 __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant__ AArgs A) {
-  constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
+  constexpr int TRW = tile_bytes<Tw>() / static_cast<int>(sizeof(Tw)) / BN;
   constexpr int TR = TRW < 256 ? TRW : 256;  // W rows per tile (16 KB of W; <= 256 TMA box rows)
   constexpr int LPR = BN / CPL;        // lanes per W row
   constexpr int RPW = 32 / LPR;        // rows per warp instruction
@@ -925,7 +933,7 @@ void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStrea
 template <typename Tw, int BN, int KR>
 bool apply_impl(const std::vector<DecJob>& jobs, double alpha, double beta, const int* skip,
                 cudaStream_t st) {
-  constexpr int TRW = kTileBytes / static_cast<int>(sizeof(Tw)) / BN;
+  constexpr int TRW = tile_bytes<Tw>() / static_cast<int>(sizeof(Tw)) / BN;
   constexpr int TR = TRW < 256 ? TRW : 256;
   const Pair& p0 = *jobs[0].pr;
   const bool use_in = beta != 0.0;
