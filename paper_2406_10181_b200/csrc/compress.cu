@@ -351,6 +351,73 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
   }
 }
 
+// fp64 fast form (no partials; c, lds, ldo, ldi even; 16-byte aligned rows):
+// one warp per (column pass of 256 doubles, output row), passes outermost so
+// the warps in flight cover every row for a few column passes (the source
+// rows of those columns come from HBM once, then L2).  Lane = 2 adjacent
+// columns per 64-column chunk (16-byte loads, 512 bytes per warp
+// instruction); entries in groups of 4 with all 16 loads of a group in flight.
+// Per column the FMA chain runs over the entries in order, exactly as
+// k_gather, so results are bitwise equal.
+constexpr int kGvChunks = 4;
+__global__ void __launch_bounds__(kGatherWarps * 32)
+    k_gather_f64v(int R, int c, int npass, const int* __restrict__ ptr, int k,
+                  const int* __restrict__ idx, const double* __restrict__ val,
+                  const double* __restrict__ src, long long lds, const double* in, long long ldi,
+                  double* out, long long ldo, double alpha, double beta) {
+  const int lane = threadIdx.x & 31;
+  const long long tasks = static_cast<long long>(R) * npass;
+  for (long long t = static_cast<long long>(blockIdx.x) * kGatherWarps + (threadIdx.x >> 5); t < tasks;
+       t += static_cast<long long>(gridDim.x) * kGatherWarps) {
+    const int pass = static_cast<int>(t / R), r = static_cast<int>(t - static_cast<long long>(pass) * R);
+    const int e0 = ptr ? __ldg(ptr + r) : r * k;
+    const int e1 = ptr ? __ldg(ptr + r + 1) : e0 + k;
+    const int c0 = pass * (64 * kGvChunks) + 2 * lane;
+    bool ok[kGvChunks];
+#pragma unroll
+    for (int q = 0; q < kGvChunks; ++q) ok[q] = c0 + 64 * q < c;
+    double2 acc[kGvChunks];
+#pragma unroll
+    for (int q = 0; q < kGvChunks; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int e = e0; e < e1; e += 4) {
+      double v[4];
+      double2 s[4][kGvChunks];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool eu = e + u < e1;
+        v[u] = eu ? __ldg(val + e + u) : 0.0;
+        const double* row = src + static_cast<long long>(eu ? __ldg(idx + e + u) : 0) * lds + c0;
+#pragma unroll
+        for (int q = 0; q < kGvChunks; ++q)
+          s[u][q] = (eu && ok[q]) ? __ldg(reinterpret_cast<const double2*>(row + 64 * q))
+                                  : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (e + u < e1) {
+#pragma unroll
+          for (int q = 0; q < kGvChunks; ++q) {
+            acc[q].x = fma(v[u], s[u][q].x, acc[q].x);
+            acc[q].y = fma(v[u], s[u][q].y, acc[q].y);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kGvChunks; ++q) {
+      if (!ok[q]) continue;
+      const int col = c0 + 64 * q;
+      double2 res = make_double2(alpha * acc[q].x, alpha * acc[q].y);
+      if (in && beta != 0.0) {
+        const double2 x = *reinterpret_cast<const double2*>(in + static_cast<long long>(r) * ldi + col);
+        res.x = fma(beta, x.x, res.x);
+        res.y = fma(beta, x.y, res.y);
+      }
+      *reinterpret_cast<double2*>(out + static_cast<long long>(r) * ldo + col) = res;
+    }
+  }
+}
+
 }  // namespace
 
 void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const void* val,
@@ -359,6 +426,20 @@ void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const vo
                    double alpha, double beta, DevBuf* partials, int* nparts, cudaStream_t st) {
   if (R <= 0 || c <= 0) {
     if (nparts) *nparts = 0;
+    return;
+  }
+  auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  if (acc == LSP_F64 && src_dt == LSP_F64 && out_dt == LSP_F64 && !partials && out &&
+      c % 2 == 0 && lds % 2 == 0 && ldo % 2 == 0 && al16(src) && al16(out) &&
+      (!in || beta == 0.0 || (ldi % 2 == 0 && al16(in)))) {
+    const int npass = ceil_div(c, 64 * kGvChunks);
+    const long long tasks = static_cast<long long>(R) * npass;
+    const int grid = static_cast<int>(std::min<long long>(ceil_div(tasks, kGatherWarps), 16LL * num_sms()));
+    if (nparts) *nparts = 0;
+    k_gather_f64v<<<grid, kGatherWarps * 32, 0, st>>>(
+        R, c, npass, ptr, k, idx, static_cast<const double*>(val), static_cast<const double*>(src), lds,
+        static_cast<const double*>(in), ldi, static_cast<double*>(out), ldo, alpha, beta);
+    after_launch("gather_f64v");
     return;
   }
   const int grid = std::min(ceil_div(R, kGatherWarps), 8 * num_sms());

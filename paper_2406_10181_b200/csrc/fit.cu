@@ -58,6 +58,9 @@ __global__ void k_dot(long long cnt, const double* __restrict__ a, const double*
 }
 
 // grad[r*k + l] += scale * ( A1[r,:].B1[pos[r*k+l],:] + A2[r,:].B2[pos[r*k+l],:] )
+// One warp per row r; lanes take 2 adjacent columns per 64-column chunk
+// (16-byte loads when d is even; ld = d); the k entries' dot products
+// share the row's A1/A2 loads.
 __global__ void k_sddmm(int R, int k, int d, const int* __restrict__ pos,
                         const double* __restrict__ A1, const double* __restrict__ B1,
                         const double* __restrict__ A2, const double* __restrict__ B2, int ld,
@@ -67,16 +70,66 @@ __global__ void k_sddmm(int R, int k, int d, const int* __restrict__ pos,
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < R; r += gridDim.x * warps) {
     const double* a1 = A1 + static_cast<long long>(r) * ld;
     const double* a2 = A2 + static_cast<long long>(r) * ld;
-    for (int l = 0; l < k; ++l) {
-      const int b = pos[static_cast<long long>(r) * k + l];
-      const double* b1 = B1 + static_cast<long long>(b) * ld;
-      const double* b2 = B2 + static_cast<long long>(b) * ld;
-      double s = 0.0;
-      for (int c = lane; c < d; c += 32) s = fma(a1[c], b1[c], fma(a2[c], b2[c], s));
+    for (int l0 = 0; l0 < k; l0 += 4) {
+      const int nl = min(4, k - l0);
+      const double* b1[4];
+      const double* b2[4];
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) grad[static_cast<long long>(r) * k + l] += scale * s;
+      for (int l = 0; l < 4; ++l) {
+        const int b = l < nl ? __ldg(pos + static_cast<long long>(r) * k + l0 + l) : 0;
+        b1[l] = B1 + static_cast<long long>(b) * ld;
+        b2[l] = B2 + static_cast<long long>(b) * ld;
+      }
+      if (d & 1) {  // odd widths: scalar columns
+        for (int c = lane; c < d; c += 32) {
+#pragma unroll
+          for (int l = 0; l < 4; ++l)
+            if (l < nl) s[l] = fma(a1[c], b1[l][c], fma(a2[c], b2[l][c], s[l]));
+        }
+      } else
+      for (int c = 2 * lane; c < d; c += 64) {
+        const double2 x1 = __ldg(reinterpret_cast<const double2*>(a1 + c));
+        const double2 x2 = __ldg(reinterpret_cast<const double2*>(a2 + c));
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          if (l >= nl) continue;
+          const double2 y1 = __ldg(reinterpret_cast<const double2*>(b1[l] + c));
+          const double2 y2 = __ldg(reinterpret_cast<const double2*>(b2[l] + c));
+          s[l] = fma(x1.x, y1.x, fma(x2.x, y2.x, s[l]));
+          s[l] = fma(x1.y, y1.y, fma(x2.y, y2.y, s[l]));
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s[l] += __shfl_xor_sync(0xffffffffu, s[l], o);
+        if (lane == 0 && l < nl) grad[static_cast<long long>(r) * k + l0 + l] += scale * s[l];
+      }
     }
+  }
+}
+
+// Deterministic per-block partials of <a, b> and <c, e> over `cnt` elements
+// (partials[block] and partials[gridDim.x + block]).
+__global__ void k_dot2(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
+                       const double* __restrict__ c, const double* __restrict__ e,
+                       double* __restrict__ partials) {
+  double s = 0.0, t = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x) {
+    s = fma(a[i], b[i], s);
+    t = fma(c[i], e[i], t);
+  }
+  __shared__ double red[2][256];
+  red[0][threadIdx.x] = s;
+  red[1][threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int i = 0; i < 256; ++i) x += red[0][i], y += red[1][i];
+    partials[blockIdx.x] = x;
+    partials[gridDim.x + blockIdx.x] = y;
   }
 }
 
@@ -223,11 +276,9 @@ struct FitEngine {
   int m, n, d, r, T;
   cudaStream_t st;
   std::unique_ptr<lsp_projector_s> P, Q;
-  lsp_pair_s pq;   // (P, Q): stage 1 on G -> Z^T
-  lsp_pair_s qp;   // (Q, P): stage 1 on G^T -> X
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
   std::vector<double> gnorm2;
-  DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, parts;
+  DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, xT, z, zt, parts, lparts;
 
   FitEngine(Pair& pr, const void* const* targets, int t, long long ld, lsp_dtype dt,
             cudaStream_t stream)
@@ -237,8 +288,6 @@ struct FitEngine {
     require(ld >= n, "fit: target leading dimension smaller than columns");
     P = shadow64(*pr.p, pr.p->h_val);
     Q = shadow64(*pr.q, pr.q->h_val);
-    pq.p = P.get(), pq.q = Q.get(), pq.m = m, pq.n = n, pq.d = d, pq.compute = LSP_F64;
-    qp.p = Q.get(), qp.q = P.get(), qp.m = n, qp.n = m, qp.d = d, qp.compute = LSP_F64;
     const size_t mn = static_cast<size_t>(m) * n;
     g.resize(t);
     gT.resize(t);
@@ -257,8 +306,12 @@ struct FitEngine {
     const size_t ms = static_cast<size_t>(m) * d * 8, ns = static_cast<size_t>(n) * d * 8;
     u.ensure(ms);
     w1.ensure(ms);
+    x.ensure(ms);
+    xT.ensure(ms);
     v.ensure(ns);
     qs.ensure(ns);
+    zt.ensure(ns);
+    z.ensure(ns);
   }
 
   void set_values(const std::vector<double>& pv, const std::vector<double>& qv) {
@@ -266,20 +319,54 @@ struct FitEngine {
     set_values64(*Q, qv, st);
   }
 
-  // |b_i|^2 = |P S Q^T - G_i|^2 for target i, evaluated directly (no
-  // cancellation): compress, then the decompress kernel in sum-of-squares mode
-  // with in = G, beta = -1 (nothing m x n is written).
-  double bias2(int i) {
-    compress_T(pq, g[i].p, n, LSP_F64, sT.p, st);
-    int np = 0;
-    launch_decompress(pq, sT.p, g[i].p, n, nullptr, 0, LSP_F64, 1.0, -1.0, nullptr, &parts,
-                      &np, st);
-    return reduce_partials_sync(parts.as<double>(), np, st);
+  // S^T = (P^T G_i Q)^T through row gathers: Z = P^T G_i (d x n, CSC of P),
+  // Z^T (n x d) by a transpose, S^T = Q^T Z^T (CSC of Q).  Per output entry the
+  // sums run over the CSC rows in ascending order, as stage 1 / stage 2 do.
+  void compress(int i) {
+    csc_gather(*P, g[i].as<double>(), n, z.as<double>(), st);      // Z   (d x n)
+    launch_transpose(d, n, z.p, n, zt.p, d, LSP_F64, st);          // Z^T (n x d)
+    csc_gather(*Q, zt.as<double>(), d, sT.as<double>(), st);       // S^T (d x d)
   }
 
-  // Gradient chain for target i: S^T, Z^T (pq.zt), A1, V, D^T.
+  // |b_i|^2 = |P S Q^T - G_i|^2 = |G_i|^2 - 2 |S|^2 + <Gp S, S Gq>  (S = P^T G_i Q,
+  // so <P S Q^T, G_i> = |S|^2 and |P S Q^T|^2 = <Gp S Gq, S>).  Enqueues the
+  // two d x d dot products' partials into lparts slot i (no host sync).
+  void bias2_enqueue(int i) {
+    compress(i);
+    launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);          // S
+    csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S
+    csc_gather(*P, u.as<double>(), d, a1.as<double>(), st);        // A1 = Gp S
+    csr_gather(*Q, sT.as<double>(), d, qs.as<double>(), st);       // Q S^T
+    csc_gather(*Q, qs.as<double>(), d, a2T.as<double>(), st);      // A2^T = Gq S^T
+    launch_transpose(d, d, a2T.p, d, a2.p, d, LSP_F64, st);        // A2 = S Gq
+    k_dot2<<<kRedBlocks, 256, 0, st>>>(static_cast<long long>(d) * d, a1.as<double>(), a2.as<double>(),
+                                       sT.as<double>(), sT.as<double>(),
+                                       lparts.as<double>() + static_cast<size_t>(i) * 2 * kRedBlocks);
+    after_launch("dot2");
+  }
+  // all targets' |b_i|^2 with one synchronisation (clamped at 0: the identity
+  // can round below zero for an exactly representable target)
+  std::vector<double> bias2_all() {
+    lparts.ensure(static_cast<size_t>(T) * 2 * kRedBlocks * sizeof(double));
+    for (int i = 0; i < T; ++i) bias2_enqueue(i);
+    std::vector<double> h(static_cast<size_t>(T) * 2 * kRedBlocks);
+    LSP_CUDA(cudaMemcpyAsync(h.data(), lparts.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    LSP_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> out(T);
+    for (int i = 0; i < T; ++i) {
+      double ag = 0.0, ss = 0.0;
+      for (int b = 0; b < kRedBlocks; ++b) {
+        ag += h[static_cast<size_t>(i) * 2 * kRedBlocks + b];
+        ss += h[static_cast<size_t>(i) * 2 * kRedBlocks + kRedBlocks + b];
+      }
+      out[i] = std::max(0.0, gnorm2[i] - 2.0 * ss + ag);
+    }
+    return out;
+  }
+
+  // Gradient chain for target i: S^T, Z^T, A1, V, D^T.
   void chain(int i) {
-    compress_T(pq, g[i].p, n, LSP_F64, sT.p, st);
+    compress(i);
     launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);
     csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S     (m x d)
     csc_gather(*P, u.as<double>(), d, a1.as<double>(), st);        // A1 = P^T U   (d x d)
@@ -294,8 +381,9 @@ struct FitEngine {
     set_values(pv, qv);
     double sum = 0.0, rel = 0.0;
     int counted = 0;
+    const std::vector<double> all = bias2_all();
     for (int i = 0; i < T; ++i) {
-      const double b2 = bias2(i);
+      const double b2 = all[i];
       sum += b2;
       if (gnorm2[i] > 0.0) {
         rel += std::sqrt(b2) / std::sqrt(gnorm2[i]);
@@ -324,37 +412,24 @@ struct FitEngine {
     dgq.ensure(std::max<size_t>(qv.size() * 8, 16));
     LSP_CUDA(cudaMemsetAsync(dgp.p, 0, pv.size() * 8, st));
     LSP_CUDA(cudaMemsetAsync(dgq.p, 0, qv.size() * 8, st));
-    x.ensure(static_cast<size_t>(m) * qp.ldz() * 8);
     const double scale = 2.0 / T;
     for (int i = 0; i < T; ++i) {
-      chain(i);                                                     // S^T, Z^T (pq.zt), A1, V, D^T
+      chain(i);                                                     // S^T, Z^T, A1, V, D^T
       launch_transpose(d, d, dT.p, d, dd.p, d, LSP_F64, st);        // D
-      launch_compress_stage1(qp, gT[i].p, m, LSP_F64, x.p, st);     // X = G Q  (m x ldz)
+      csc_gather(*Q, gT[i].as<double>(), m, xT.as<double>(), st);  // X^T = Q^T G^T (d x m)
+      launch_transpose(d, m, xT.p, m, x.p, d, LSP_F64, st);         // X = G Q    (m x d)
       csr_gather(*Q, sT.as<double>(), d, qs.as<double>(), st);      // Q S^T    (n x d)
       csc_gather(*Q, qs.as<double>(), d, a2T.as<double>(), st);     // A2^T = Gq S^T
       launch_transpose(d, d, a2T.p, d, a2.p, d, LSP_F64, st);       // A2 = S Gq
       csr_gather(*P, a2.as<double>(), d, w1.as<double>(), st);      // W1 = P A2 (m x d)
-      // X and Z^T have leading dimension ldz (= round_up(d,4)); compact them to d.
-      const double* xd = x.as<double>();
-      const double* zd = pq.zt.as<double>();
-      DevBuf xc, zc;
-      if (qp.ldz() != d) {
-        xc.ensure(static_cast<size_t>(m) * d * 8);
-        zc.ensure(static_cast<size_t>(n) * d * 8);
-        launch_convert2d(m, d, xd, qp.ldz(), LSP_F64, xc.p, d, LSP_F64, st);
-        launch_convert2d(n, d, zd, pq.ldz(), LSP_F64, zc.p, d, LSP_F64, st);
-        xd = xc.as<double>();
-        zd = zc.as<double>();
-      }
       k_sddmm<<<egrid(static_cast<long long>(m) * 32), 256, 0, st>>>(
-          m, r, d, P->pos.as<int>(), w1.as<double>(), s.as<double>(), xd, dd.as<double>(), d,
+          m, r, d, P->pos.as<int>(), w1.as<double>(), s.as<double>(), x.as<double>(), dd.as<double>(), d,
           scale, dgp.as<double>());
       after_launch("sddmm_p");
       k_sddmm<<<egrid(static_cast<long long>(n) * 32), 256, 0, st>>>(
-          n, r, d, Q->pos.as<int>(), v.as<double>(), sT.as<double>(), zd, dT.as<double>(), d,
+          n, r, d, Q->pos.as<int>(), v.as<double>(), sT.as<double>(), zt.as<double>(), dT.as<double>(), d,
           scale, dgq.as<double>());
       after_launch("sddmm_q");
-      LSP_CUDA(cudaStreamSynchronize(st));
     }
     gp.resize(pv.size());
     gq.resize(qv.size());
