@@ -852,7 +852,13 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
 
 template <int BN, int KR>
 void build_y_impl(const std::vector<DecJob>& jobs_in, const int* skip, cudaStream_t st) {
-  const std::vector<DecJob>& jobs = jobs_in;
+  // Build the group's Y blocks in reverse matrix order: the apply walks the
+  // matrices forward, so the blocks it needs first are the ones written last
+  // (evict-last) and still L2-resident when a layer's Y exceeds the L2.
+  // LSP_BUILD_Y_REVERSE=0 keeps the forward order (results are identical).
+  const char* rev_env = std::getenv("LSP_BUILD_Y_REVERSE");
+  const bool rev = !(rev_env && rev_env[0] == '0');
+  const std::vector<DecJob> jobs = rev ? std::vector<DecJob>(jobs_in.rbegin(), jobs_in.rend()) : jobs_in;
   const Pair& p0 = *jobs[0].pr;
   const char* env = std::getenv("LSP_BUILD_Y_GLOBAL");
   // the shared-memory build stages Delta^T rows with 16-byte loads: d % 4 == 0
