@@ -781,21 +781,31 @@ __global__ void __launch_bounds__(kAThreads, 1) k_apply_y(const __grid_constant_
           if (USE_IN) res = fmaf(beta, lds_w<Tw>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw))), res);
           return cvt<Tw>(res);
         } else {
+          // packed FMUL2 / FFMA2 (two IEEE operations per instruction, same
+          // per-column order as CPL = 1)
           FV<CPL> acc = lds_yv<CPL>(y_lane + pp[0]);
+          auto pairs = [&](auto&& op) {
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) acc.v[c] = vv[0] * acc.v[c];
+            for (int c = 0; c < CPL; c += 2) {
+              const float2 r = op(c, make_float2(acc.v[c], acc.v[c + 1]));
+              acc.v[c] = r.x;
+              acc.v[c + 1] = r.y;
+            }
+          };
+          pairs([&](int, float2 a) { return __fmul2_rn(make_float2(vv[0], vv[0]), a); });
 #pragma unroll
           for (int l = 1; l < KR; ++l) {
             const FV<CPL> y = lds_yv<CPL>(y_lane + pp[l]);
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) acc.v[c] = fmaf(vv[l], y.v[c], acc.v[c]);
+            pairs([&](int c, float2 a) {
+              return __ffma2_rn(make_float2(vv[l], vv[l]), make_float2(y.v[c], y.v[c + 1]), a);
+            });
           }
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) acc.v[c] = alpha * acc.v[c];
+          pairs([&](int, float2 a) { return __fmul2_rn(make_float2(alpha, alpha), a); });
           if (USE_IN) {
             const FV<CPL> w = lds_wv<Tw, CPL>(wq + v * kq * BN * static_cast<unsigned>(sizeof(Tw)));
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) acc.v[c] = fmaf(beta, w.v[c], acc.v[c]);
+            pairs([&](int c, float2 a) {
+              return __ffma2_rn(make_float2(beta, beta), make_float2(w.v[c], w.v[c + 1]), a);
+            });
           }
           return acc;
         }

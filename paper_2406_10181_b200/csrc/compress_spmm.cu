@@ -214,9 +214,15 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
       --cleft;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        // packed FFMA2: two IEEE fmas per instruction, same per-column chain
         const float p = __uint_as_float(en[u].y);
+        const float2 pp = make_float2(p, p);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = fmaf(p, g[u][c], acc[c]);
+        for (int c = 0; c < CPL; c += 2) {
+          const float2 r = __ffma2_rn(pp, make_float2(g[u][c], g[u][c + 1]), make_float2(acc[c], acc[c + 1]));
+          acc[c] = r.x;
+          acc[c + 1] = r.y;
+        }
       }
     };
     if constexpr (U * CPL <= 32) {  // registers for two batches: double-buffered
