@@ -133,6 +133,14 @@ __global__ void k_dot2(long long cnt, const double* __restrict__ a, const double
   }
 }
 
+// out = a - t*b + t^2*c  (S^T along the line-search ray, see FitEngine::prepare_line)
+__global__ void k_poly2(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
+                        const double* __restrict__ c, double t, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = fma(t * t, c[i], fma(-t, b[i], a[i]));
+}
+
 // out (da x db, row-major) = A^T B for two projectors over the same rows, in
 // the reference's summation order (rows ascending per output entry,
 // subspace_opt.cpp:59-70), without contraction so fp64 results match it.
@@ -275,10 +283,11 @@ struct FitEngine {
   Pair& orig;
   int m, n, d, r, T;
   cudaStream_t st;
-  std::unique_ptr<lsp_projector_s> P, Q;
+  std::unique_ptr<lsp_projector_s> P, Q, Pd, Qd;  // Pd, Qd: the descent direction's values
+  std::vector<DevBuf> s0T, s1T, s2T;                // per target: S^T(t) = s0T - t s1T + t^2 s2T
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
   std::vector<double> gnorm2;
-  DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, xT, z, zt, parts, lparts;
+  DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, xT, z, zt, zdt, parts, lparts;
 
   FitEngine(Pair& pr, const void* const* targets, int t, long long ld, lsp_dtype dt,
             cudaStream_t stream)
@@ -288,6 +297,8 @@ struct FitEngine {
     require(ld >= n, "fit: target leading dimension smaller than columns");
     P = shadow64(*pr.p, pr.p->h_val);
     Q = shadow64(*pr.q, pr.q->h_val);
+    Pd = shadow64(*pr.p, pr.p->h_val);
+    Qd = shadow64(*pr.q, pr.q->h_val);
     const size_t mn = static_cast<size_t>(m) * n;
     g.resize(t);
     gT.resize(t);
@@ -333,6 +344,39 @@ struct FitEngine {
   // two d x d dot products' partials into lparts slot i (no host sync).
   void bias2_enqueue(int i) {
     compress(i);
+    bias2_from_sT(i);
+  }
+  // Line search along (P, Q) - t (dP, dQ): the trial values are the current
+  // ones minus t times the gradient, and S is bilinear in (P, Q), so
+  //   S(t) = S0 - t S1 + t^2 S2,  S0 = P^T G Q,  S1 = dP^T G Q + P^T G dQ,
+  //   S2 = dP^T G dQ
+  // per target, computed once per GD step (two passes over G instead of one
+  // per trial); a trial then costs only the d-wide gathers of bias2_from_sT.
+  void prepare_line(const std::vector<double>& pv, const std::vector<double>& qv,
+                    const std::vector<double>& gp, const std::vector<double>& gq) {
+    set_values(pv, qv);
+    set_values64(*Pd, gp, st);
+    set_values64(*Qd, gq, st);
+    const size_t dd2 = static_cast<size_t>(d) * d * 8;
+    s0T.resize(T);
+    s1T.resize(T);
+    s2T.resize(T);
+    zdt.ensure(static_cast<size_t>(n) * d * 8);
+    for (int i = 0; i < T; ++i) {
+      for (DevBuf* b : {&s0T[i], &s1T[i], &s2T[i]}) b->ensure(dd2);
+      csc_gather(*P, g[i].as<double>(), n, z.as<double>(), st);      // Z0  = P^T G
+      launch_transpose(d, n, z.p, n, zt.p, d, LSP_F64, st);
+      csc_gather(*Pd, g[i].as<double>(), n, z.as<double>(), st);     // Zd  = dP^T G
+      launch_transpose(d, n, z.p, n, zdt.p, d, LSP_F64, st);
+      csc_gather(*Q, zt.as<double>(), d, s0T[i].as<double>(), st);   // S0^T
+      csc_gather(*Q, zdt.as<double>(), d, s1T[i].as<double>(), st);  // (dP^T G Q)^T
+      csc_gather(*Qd, zt.as<double>(), d, s1T[i].as<double>(), st, 1.0, s1T[i].as<double>());  // + (P^T G dQ)^T
+      csc_gather(*Qd, zdt.as<double>(), d, s2T[i].as<double>(), st); // S2^T
+    }
+  }
+
+  // |b_i|^2 from S^T already in sT (the rest of bias2_enqueue)
+  void bias2_from_sT(int i) {
     launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);          // S
     csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S
     csc_gather(*P, u.as<double>(), d, a1.as<double>(), st);        // A1 = Gp S
@@ -344,11 +388,23 @@ struct FitEngine {
                                        lparts.as<double>() + static_cast<size_t>(i) * 2 * kRedBlocks);
     after_launch("dot2");
   }
+
   // all targets' |b_i|^2 with one synchronisation (clamped at 0: the identity
-  // can round below zero for an exactly representable target)
-  std::vector<double> bias2_all() {
+  // can round below zero for an exactly representable target); line_t >= 0:
+  // S^T from the prepared line-search polynomial instead of a pass over G
+  std::vector<double> bias2_all(double line_t = -1.0) {
     lparts.ensure(static_cast<size_t>(T) * 2 * kRedBlocks * sizeof(double));
-    for (int i = 0; i < T; ++i) bias2_enqueue(i);
+    for (int i = 0; i < T; ++i) {
+      if (line_t >= 0.0) {
+        const long long dd = static_cast<long long>(d) * d;
+        k_poly2<<<egrid(dd), 256, 0, st>>>(dd, s0T[i].as<double>(), s1T[i].as<double>(),
+                                           s2T[i].as<double>(), line_t, sT.as<double>());
+        after_launch("poly2");
+        bias2_from_sT(i);
+      } else {
+        bias2_enqueue(i);
+      }
+    }
     std::vector<double> h(static_cast<size_t>(T) * 2 * kRedBlocks);
     LSP_CUDA(cudaMemcpyAsync(h.data(), lparts.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     LSP_CUDA(cudaStreamSynchronize(st));
@@ -377,11 +433,11 @@ struct FitEngine {
 
   // loss = mean_t |b_t|^2 + reg ; rel = mean over nonzero targets of |b_t|/|G_t|
   void loss(const std::vector<double>& pv, const std::vector<double>& qv,
-            const lsp_fit_config& cfg, double* loss_out, double* rel_out) {
+            const lsp_fit_config& cfg, double* loss_out, double* rel_out, double line_t = -1.0) {
     set_values(pv, qv);
     double sum = 0.0, rel = 0.0;
     int counted = 0;
-    const std::vector<double> all = bias2_all();
+    const std::vector<double> all = bias2_all(line_t);
     for (int i = 0; i < T; ++i) {
       const double b2 = all[i];
       sum += b2;
@@ -534,13 +590,14 @@ int lsp_fit(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_
     std::vector<double> gp, gq, tp(pv.size()), tq(qv.size());
     for (int step = 0; step < budget && !success; ++step) {
       fe.gradient(pv, qv, c, gp, gq);
+      fe.prepare_line(pv, qv, gp, gq);
       double trial_step = c.step_size;
       bool accepted = false;
       for (int halving = 0; halving < 40; ++halving) {
         for (size_t i = 0; i < pv.size(); ++i) tp[i] = pv[i] - trial_step * gp[i];
         for (size_t i = 0; i < qv.size(); ++i) tq[i] = qv[i] - trial_step * gq[i];
         double tl = 0.0, trel = 0.0;
-        fe.loss(tp, tq, c, &tl, &trel);
+        fe.loss(tp, tq, c, &tl, &trel, trial_step);
         if (std::isfinite(tl) && tl < loss) {
           pv.swap(tp);
           qv.swap(tq);
