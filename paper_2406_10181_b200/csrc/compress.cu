@@ -360,16 +360,25 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
 // Per column the FMA chain runs over the entries in order, exactly as
 // k_gather, so results are bitwise equal.
 constexpr int kGvChunks = 4;
+// nb > 1: a batch of independent gathers through the same projector, operand
+// b at src + b*sbs, in + b*ibs, out + b*obs (one launch for every target of a fit).
 __global__ void __launch_bounds__(kGatherWarps * 32)
     k_gather_f64v(int R, int c, int npass, const int* __restrict__ ptr, int k,
                   const int* __restrict__ idx, const double* __restrict__ val,
-                  const double* __restrict__ src, long long lds, const double* in, long long ldi,
-                  double* out, long long ldo, double alpha, double beta) {
+                  const double* __restrict__ src_base, long long lds, const double* in_base, long long ldi,
+                  double* out_base, long long ldo, double alpha, double beta, int nb, long long sbs,
+                  long long ibs, long long obs) {
   const int lane = threadIdx.x & 31;
-  const long long tasks = static_cast<long long>(R) * npass;
+  const long long per = static_cast<long long>(R) * npass;
+  const long long tasks = per * nb;
   for (long long t = static_cast<long long>(blockIdx.x) * kGatherWarps + (threadIdx.x >> 5); t < tasks;
        t += static_cast<long long>(gridDim.x) * kGatherWarps) {
-    const int pass = static_cast<int>(t / R), r = static_cast<int>(t - static_cast<long long>(pass) * R);
+    const int bi = static_cast<int>(t / per);
+    const long long tb = t - bi * per;
+    const double* __restrict__ src = src_base + bi * sbs;
+    const double* in = in_base ? in_base + bi * ibs : nullptr;
+    double* out = out_base + bi * obs;
+    const int pass = static_cast<int>(tb / R), r = static_cast<int>(tb - static_cast<long long>(pass) * R);
     const int e0 = ptr ? __ldg(ptr + r) : r * k;
     const int e1 = ptr ? __ldg(ptr + r + 1) : e0 + k;
     const int c0 = pass * (64 * kGvChunks) + 2 * lane;
@@ -420,6 +429,24 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
 
 }  // namespace
 
+void launch_gather_f64_batch(int R, int c, const int* ptr, int k, const int* idx, const double* val,
+                             const double* src, long long lds, long long sbs, const double* in,
+                             long long ldi, long long ibs, double* out, long long ldo, long long obs,
+                             int nb, double alpha, double beta, cudaStream_t st) {
+  if (R <= 0 || c <= 0 || nb <= 0) return;
+  require(c % 2 == 0 && lds % 2 == 0 && ldo % 2 == 0 && sbs % 2 == 0 && obs % 2 == 0 &&
+              (!in || (ldi % 2 == 0 && ibs % 2 == 0)) &&
+              reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+              (!in || reinterpret_cast<uintptr_t>(in) % 16 == 0),
+          "gather_f64: 16-byte aligned rows of an even width required");
+  const int npass = ceil_div(c, 64 * kGvChunks);
+  const long long tasks = static_cast<long long>(R) * npass * nb;
+  const int grid = static_cast<int>(std::min<long long>(ceil_div(tasks, kGatherWarps), 16LL * num_sms()));
+  k_gather_f64v<<<grid, kGatherWarps * 32, 0, st>>>(R, c, npass, ptr, k, idx, val, src, lds, in, ldi, out,
+                                                     ldo, alpha, beta, nb, sbs, ibs, obs);
+  after_launch("gather_f64v");
+}
+
 void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const void* val,
                    lsp_dtype acc, const void* src, long long lds, lsp_dtype src_dt,
                    const void* in, long long ldi, void* out, long long ldo, lsp_dtype out_dt,
@@ -432,14 +459,10 @@ void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const vo
   if (acc == LSP_F64 && src_dt == LSP_F64 && out_dt == LSP_F64 && !partials && out &&
       c % 2 == 0 && lds % 2 == 0 && ldo % 2 == 0 && al16(src) && al16(out) &&
       (!in || beta == 0.0 || (ldi % 2 == 0 && al16(in)))) {
-    const int npass = ceil_div(c, 64 * kGvChunks);
-    const long long tasks = static_cast<long long>(R) * npass;
-    const int grid = static_cast<int>(std::min<long long>(ceil_div(tasks, kGatherWarps), 16LL * num_sms()));
     if (nparts) *nparts = 0;
-    k_gather_f64v<<<grid, kGatherWarps * 32, 0, st>>>(
-        R, c, npass, ptr, k, idx, static_cast<const double*>(val), static_cast<const double*>(src), lds,
-        static_cast<const double*>(in), ldi, static_cast<double*>(out), ldo, alpha, beta);
-    after_launch("gather_f64v");
+    launch_gather_f64_batch(R, c, ptr, k, idx, static_cast<const double*>(val),
+                            static_cast<const double*>(src), lds, 0, (in && beta != 0.0) ? static_cast<const double*>(in) : nullptr,
+                            ldi, 0, static_cast<double*>(out), ldo, 0, 1, alpha, beta, st);
     return;
   }
   const int grid = std::min(ceil_div(R, kGatherWarps), 8 * num_sms());
@@ -465,8 +488,10 @@ void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const vo
 namespace {
 template <typename T>
 __global__ void k_transpose(int rows, int cols, const T* __restrict__ src, long long lds,
-                            T* __restrict__ dst, long long ldd) {
+                            T* __restrict__ dst, long long ldd, long long sbs, long long dbs) {
   __shared__ T tile[32][33];
+  src += blockIdx.z * sbs;  // batch (gridDim.z operands at fixed strides)
+  dst += blockIdx.z * dbs;
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int y = threadIdx.y; y < 32; y += 8) {
     const int r = by + y, c = bx + threadIdx.x;
@@ -486,8 +511,16 @@ void launch_transpose(int rows, int cols, const void* src, long long lds, void* 
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32)), block(32, 8);
   LSP_DISPATCH_STORAGE(dt, T, {
     k_transpose<T><<<grid, block, 0, st>>>(rows, cols, static_cast<const T*>(src), lds,
-                                           static_cast<T*>(dst), ldd);
+                                           static_cast<T*>(dst), ldd, 0, 0);
   })
+  after_launch("transpose");
+}
+
+void launch_transpose_batch(int rows, int cols, const double* src, long long lds, long long sbs,
+                            double* dst, long long ldd, long long dbs, int nb, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || nb <= 0) return;
+  dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32), nb), block(32, 8);
+  k_transpose<double><<<grid, block, 0, st>>>(rows, cols, src, lds, dst, ldd, sbs, dbs);
   after_launch("transpose");
 }
 

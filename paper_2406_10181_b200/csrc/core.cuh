@@ -199,6 +199,13 @@ void launch_gather(int R, int c, const int* ptr, int k, const int* idx, const vo
                    lsp_dtype acc, const void* src, long long lds, lsp_dtype src_dt,
                    const void* in, long long ldi, void* out, long long ldo, lsp_dtype out_dt,
                    double alpha, double beta, DevBuf* partials, int* nparts, cudaStream_t st);
+// fp64 batch of row gathers through one projector (operand b at base + b * stride)
+void launch_gather_f64_batch(int R, int c, const int* ptr, int k, const int* idx, const double* val,
+                             const double* src, long long lds, long long sbs, const double* in,
+                             long long ldi, long long ibs, double* out, long long ldo, long long obs,
+                             int nb, double alpha, double beta, cudaStream_t st);
+void launch_transpose_batch(int rows, int cols, const double* src, long long lds, long long sbs,
+                            double* dst, long long ldd, long long dbs, int nb, cudaStream_t st);
 void launch_transpose(int rows, int cols, const void* src, long long lds, void* dst,
                       long long ldd, lsp_dtype dt, cudaStream_t st);
 // Fused decompress: out = beta*in + alpha * P (delta) Q^T, delta given as delta^T.

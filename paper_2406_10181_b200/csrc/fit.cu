@@ -112,9 +112,13 @@ __global__ void k_sddmm(int R, int k, int d, const int* __restrict__ pos,
 
 // Deterministic per-block partials of <a, b> and <c, e> over `cnt` elements
 // (partials[block] and partials[gridDim.x + block]).
+// Batched over blockIdx.y: operands at + y*cnt, partials at + y*2*gridDim.x.
 __global__ void k_dot2(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
                        const double* __restrict__ c, const double* __restrict__ e,
                        double* __restrict__ partials) {
+  const long long off = static_cast<long long>(blockIdx.y) * cnt;
+  a += off, b += off, c += off, e += off;
+  partials += static_cast<long long>(blockIdx.y) * 2 * gridDim.x;
   double s = 0.0, t = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
        i += (long long)gridDim.x * blockDim.x) {
@@ -284,7 +288,9 @@ struct FitEngine {
   int m, n, d, r, T;
   cudaStream_t st;
   std::unique_ptr<lsp_projector_s> P, Q, Pd, Qd;  // Pd, Qd: the descent direction's values
-  std::vector<DevBuf> s0T, s1T, s2T;                // per target: S^T(t) = s0T - t s1T + t^2 s2T
+  // per target (contiguous, target-major): S^T(t) = s0T - t s1T + t^2 s2T, and the
+  // batched loss intermediates
+  DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, bqs, ba2T, ba2;
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
   std::vector<double> gnorm2;
   DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, xT, z, zt, zdt, parts, lparts;
@@ -339,53 +345,72 @@ struct FitEngine {
     csc_gather(*Q, zt.as<double>(), d, sT.as<double>(), st);       // S^T (d x d)
   }
 
-  // |b_i|^2 = |P S Q^T - G_i|^2 = |G_i|^2 - 2 |S|^2 + <Gp S, S Gq>  (S = P^T G_i Q,
-  // so <P S Q^T, G_i> = |S|^2 and |P S Q^T|^2 = <Gp S Gq, S>).  Enqueues the
-  // two d x d dot products' partials into lparts slot i (no host sync).
-  void bias2_enqueue(int i) {
-    compress(i);
-    bias2_from_sT(i);
-  }
   // Line search along (P, Q) - t (dP, dQ): the trial values are the current
   // ones minus t times the gradient, and S is bilinear in (P, Q), so
   //   S(t) = S0 - t S1 + t^2 S2,  S0 = P^T G Q,  S1 = dP^T G Q + P^T G dQ,
   //   S2 = dP^T G dQ
   // per target, computed once per GD step (two passes over G instead of one
-  // per trial); a trial then costs only the d-wide gathers of bias2_from_sT.
+  // per trial); a trial then costs only the d-wide gathers of bias2_from_bsT.
   void prepare_line(const std::vector<double>& pv, const std::vector<double>& qv,
                     const std::vector<double>& gp, const std::vector<double>& gq) {
     set_values(pv, qv);
     set_values64(*Pd, gp, st);
     set_values64(*Qd, gq, st);
-    const size_t dd2 = static_cast<size_t>(d) * d * 8;
-    s0T.resize(T);
-    s1T.resize(T);
-    s2T.resize(T);
+    const size_t dd = static_cast<size_t>(d) * d;
+    for (DevBuf* b : {&s0T, &s1T, &s2T}) b->ensure(T * dd * 8);
     zdt.ensure(static_cast<size_t>(n) * d * 8);
     for (int i = 0; i < T; ++i) {
-      for (DevBuf* b : {&s0T[i], &s1T[i], &s2T[i]}) b->ensure(dd2);
+      double* s0 = s0T.as<double>() + i * dd;
+      double* s1 = s1T.as<double>() + i * dd;
+      double* s2 = s2T.as<double>() + i * dd;
       csc_gather(*P, g[i].as<double>(), n, z.as<double>(), st);      // Z0  = P^T G
       launch_transpose(d, n, z.p, n, zt.p, d, LSP_F64, st);
       csc_gather(*Pd, g[i].as<double>(), n, z.as<double>(), st);     // Zd  = dP^T G
       launch_transpose(d, n, z.p, n, zdt.p, d, LSP_F64, st);
-      csc_gather(*Q, zt.as<double>(), d, s0T[i].as<double>(), st);   // S0^T
-      csc_gather(*Q, zdt.as<double>(), d, s1T[i].as<double>(), st);  // (dP^T G Q)^T
-      csc_gather(*Qd, zt.as<double>(), d, s1T[i].as<double>(), st, 1.0, s1T[i].as<double>());  // + (P^T G dQ)^T
-      csc_gather(*Qd, zdt.as<double>(), d, s2T[i].as<double>(), st); // S2^T
+      csc_gather(*Q, zt.as<double>(), d, s0, st);                     // S0^T
+      csc_gather(*Q, zdt.as<double>(), d, s1, st);                    // (dP^T G Q)^T
+      csc_gather(*Qd, zt.as<double>(), d, s1, st, 1.0, s1);           // + (P^T G dQ)^T
+      csc_gather(*Qd, zdt.as<double>(), d, s2, st);                   // S2^T
     }
   }
 
-  // |b_i|^2 from S^T already in sT (the rest of bias2_enqueue)
-  void bias2_from_sT(int i) {
-    launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);          // S
-    csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S
-    csc_gather(*P, u.as<double>(), d, a1.as<double>(), st);        // A1 = Gp S
-    csr_gather(*Q, sT.as<double>(), d, qs.as<double>(), st);       // Q S^T
-    csc_gather(*Q, qs.as<double>(), d, a2T.as<double>(), st);      // A2^T = Gq S^T
-    launch_transpose(d, d, a2T.p, d, a2.p, d, LSP_F64, st);        // A2 = S Gq
-    k_dot2<<<kRedBlocks, 256, 0, st>>>(static_cast<long long>(d) * d, a1.as<double>(), a2.as<double>(),
-                                       sT.as<double>(), sT.as<double>(),
-                                       lparts.as<double>() + static_cast<size_t>(i) * 2 * kRedBlocks);
+  // |b_i|^2 = |P S Q^T - G_i|^2 = |G_i|^2 - 2 |S|^2 + <Gp S, S Gq>  (S = P^T G_i Q,
+  // so <P S Q^T, G_i> = |S|^2 and |P S Q^T|^2 = <Gp S Gq, S>), for every target
+  // from S^T in bsT (T x d x d): one batched launch per product, the two d x d
+  // dot products' partials of target i in lparts slot i (no host sync)
+  // batch of T row gathers through projector X (CSR rows when csr, else CSC
+  // bins) from src + i*sbs into out + i*obs; odd widths go target by target
+  // through the generic gather
+  void gather_batch(const Projector& X, bool csr, const double* src, long long sbs, double* out,
+                    long long obs) {
+    const int R = csr ? X.n_rows : X.d;
+    const int* ptr = csr ? nullptr : X.csc_ptr.as<int>();
+    const int k = csr ? X.r : 0;
+    const int* idx = csr ? X.pos.as<int>() : X.csc_row.as<int>();
+    const double* val = csr ? X.val.as<double>() : X.csc_val.as<double>();
+    if (d % 2 == 0) {
+      launch_gather_f64_batch(R, d, ptr, k, idx, val, src, d, sbs, nullptr, 0, 0, out, d, obs, T, 1.0, 0.0, st);
+      return;
+    }
+    for (int i = 0; i < T; ++i)
+      launch_gather(R, d, ptr, k, idx, val, LSP_F64, src + i * sbs, d, LSP_F64, nullptr, 0, out + i * obs, d,
+                    LSP_F64, 1.0, 0.0, nullptr, nullptr, st);
+  }
+
+  void bias2_from_bsT() {
+    const size_t dd = static_cast<size_t>(d) * d, md = static_cast<size_t>(m) * d,
+                 nd = static_cast<size_t>(n) * d;
+    bs.ensure(T * dd * 8), ba1.ensure(T * dd * 8), ba2T.ensure(T * dd * 8), ba2.ensure(T * dd * 8);
+    bu.ensure(T * md * 8), bqs.ensure(T * nd * 8);
+    const double* sTp = bsT.as<double>();
+    launch_transpose_batch(d, d, sTp, d, dd, bs.as<double>(), d, dd, T, st);              // S
+    gather_batch(*P, true, bs.as<double>(), dd, bu.as<double>(), md);      // U    = P S
+    gather_batch(*P, false, bu.as<double>(), md, ba1.as<double>(), dd);    // A1   = Gp S
+    gather_batch(*Q, true, sTp, dd, bqs.as<double>(), nd);                 // Q S^T
+    gather_batch(*Q, false, bqs.as<double>(), nd, ba2T.as<double>(), dd);  // A2^T = Gq S^T
+    launch_transpose_batch(d, d, ba2T.as<double>(), d, dd, ba2.as<double>(), d, dd, T, st);  // A2 = S Gq
+    k_dot2<<<dim3(kRedBlocks, T), 256, 0, st>>>(static_cast<long long>(dd), ba1.as<double>(), ba2.as<double>(),
+                                                sTp, sTp, lparts.as<double>());
     after_launch("dot2");
   }
 
@@ -394,17 +419,20 @@ struct FitEngine {
   // S^T from the prepared line-search polynomial instead of a pass over G
   std::vector<double> bias2_all(double line_t = -1.0) {
     lparts.ensure(static_cast<size_t>(T) * 2 * kRedBlocks * sizeof(double));
-    for (int i = 0; i < T; ++i) {
-      if (line_t >= 0.0) {
-        const long long dd = static_cast<long long>(d) * d;
-        k_poly2<<<egrid(dd), 256, 0, st>>>(dd, s0T[i].as<double>(), s1T[i].as<double>(),
-                                           s2T[i].as<double>(), line_t, sT.as<double>());
-        after_launch("poly2");
-        bias2_from_sT(i);
-      } else {
-        bias2_enqueue(i);
+    const size_t dd = static_cast<size_t>(d) * d;
+    bsT.ensure(T * dd * 8);
+    if (line_t >= 0.0) {
+      const long long cnt = static_cast<long long>(T * dd);
+      k_poly2<<<egrid(cnt), 256, 0, st>>>(cnt, s0T.as<double>(), s1T.as<double>(), s2T.as<double>(), line_t,
+                                          bsT.as<double>());
+      after_launch("poly2");
+    } else {
+      for (int i = 0; i < T; ++i) {
+        compress(i);
+        LSP_CUDA(cudaMemcpyAsync(bsT.as<double>() + i * dd, sT.p, dd * 8, cudaMemcpyDeviceToDevice, st));
       }
     }
+    bias2_from_bsT();
     std::vector<double> h(static_cast<size_t>(T) * 2 * kRedBlocks);
     LSP_CUDA(cudaMemcpyAsync(h.data(), lparts.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     LSP_CUDA(cudaStreamSynchronize(st));
