@@ -291,6 +291,7 @@ struct FitEngine {
   // per target (contiguous, target-major): S^T(t) = s0T - t s1T + t^2 s2T, and the
   // batched loss intermediates
   DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, bqs, ba2T, ba2;
+  DevBuf zt_all;  // per target Z^T = G^T P of the last gradient (reused by prepare_line)
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
   std::vector<double> gnorm2;
   DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, xT, z, zt, zdt, parts, lparts;
@@ -339,10 +340,10 @@ struct FitEngine {
   // S^T = (P^T G_i Q)^T through row gathers: Z = P^T G_i (d x n, CSC of P),
   // Z^T (n x d) by a transpose, S^T = Q^T Z^T (CSC of Q).  Per output entry the
   // sums run over the CSC rows in ascending order, as stage 1 / stage 2 do.
-  void compress(int i) {
+  void compress(int i, double* ztp, double* sTp) {
     csc_gather(*P, g[i].as<double>(), n, z.as<double>(), st);      // Z   (d x n)
-    launch_transpose(d, n, z.p, n, zt.p, d, LSP_F64, st);          // Z^T (n x d)
-    csc_gather(*Q, zt.as<double>(), d, sT.as<double>(), st);       // S^T (d x d)
+    launch_transpose(d, n, z.p, n, ztp, d, LSP_F64, st);           // Z^T (n x d)
+    csc_gather(*Q, ztp, d, sTp, st);                               // S^T (d x d)
   }
 
   // Line search along (P, Q) - t (dP, dQ): the trial values are the current
@@ -351,25 +352,24 @@ struct FitEngine {
   //   S2 = dP^T G dQ
   // per target, computed once per GD step (two passes over G instead of one
   // per trial); a trial then costs only the d-wide gathers of bias2_from_bsT.
+  // Requires the gradient at (pv, qv) just before: its Z0^T and S0^T (zt_all,
+  // s0T) are reused, so a GD step makes one extra pass over each G (Zd).
   void prepare_line(const std::vector<double>& pv, const std::vector<double>& qv,
                     const std::vector<double>& gp, const std::vector<double>& gq) {
     set_values(pv, qv);
     set_values64(*Pd, gp, st);
     set_values64(*Qd, gq, st);
-    const size_t dd = static_cast<size_t>(d) * d;
-    for (DevBuf* b : {&s0T, &s1T, &s2T}) b->ensure(T * dd * 8);
-    zdt.ensure(static_cast<size_t>(n) * d * 8);
+    const size_t dd = static_cast<size_t>(d) * d, nd = static_cast<size_t>(n) * d;
+    for (DevBuf* b : {&s1T, &s2T}) b->ensure(T * dd * 8);
+    zdt.ensure(nd * 8);
     for (int i = 0; i < T; ++i) {
-      double* s0 = s0T.as<double>() + i * dd;
+      const double* z0t = zt_all.as<double>() + i * nd;
       double* s1 = s1T.as<double>() + i * dd;
       double* s2 = s2T.as<double>() + i * dd;
-      csc_gather(*P, g[i].as<double>(), n, z.as<double>(), st);      // Z0  = P^T G
-      launch_transpose(d, n, z.p, n, zt.p, d, LSP_F64, st);
       csc_gather(*Pd, g[i].as<double>(), n, z.as<double>(), st);     // Zd  = dP^T G
       launch_transpose(d, n, z.p, n, zdt.p, d, LSP_F64, st);
-      csc_gather(*Q, zt.as<double>(), d, s0, st);                     // S0^T
       csc_gather(*Q, zdt.as<double>(), d, s1, st);                    // (dP^T G Q)^T
-      csc_gather(*Qd, zt.as<double>(), d, s1, st, 1.0, s1);           // + (P^T G dQ)^T
+      csc_gather(*Qd, z0t, d, s1, st, 1.0, s1);                       // + (P^T G dQ)^T
       csc_gather(*Qd, zdt.as<double>(), d, s2, st);                   // S2^T
     }
   }
@@ -427,10 +427,7 @@ struct FitEngine {
                                           bsT.as<double>());
       after_launch("poly2");
     } else {
-      for (int i = 0; i < T; ++i) {
-        compress(i);
-        LSP_CUDA(cudaMemcpyAsync(bsT.as<double>() + i * dd, sT.p, dd * 8, cudaMemcpyDeviceToDevice, st));
-      }
+      for (int i = 0; i < T; ++i) compress(i, zt.as<double>(), bsT.as<double>() + i * dd);
     }
     bias2_from_bsT();
     std::vector<double> h(static_cast<size_t>(T) * 2 * kRedBlocks);
@@ -449,14 +446,14 @@ struct FitEngine {
   }
 
   // Gradient chain for target i: S^T, Z^T, A1, V, D^T.
-  void chain(int i) {
-    compress(i);
-    launch_transpose(d, d, sT.p, d, s.p, d, LSP_F64, st);
+  void chain(int i, double* ztp, double* sTp) {
+    compress(i, ztp, sTp);
+    launch_transpose(d, d, sTp, d, s.p, d, LSP_F64, st);
     csr_gather(*P, s.as<double>(), d, u.as<double>(), st);         // U  = P S     (m x d)
     csc_gather(*P, u.as<double>(), d, a1.as<double>(), st);        // A1 = P^T U   (d x d)
     launch_transpose(d, d, a1.p, d, a1T.p, d, LSP_F64, st);
     csr_gather(*Q, a1T.as<double>(), d, v.as<double>(), st);       // V  = Q A1^T  (n x d)
-    csc_gather(*Q, v.as<double>(), d, dT.as<double>(), st, -2.0, sT.as<double>());  // D^T
+    csc_gather(*Q, v.as<double>(), d, dT.as<double>(), st, -2.0, sTp);            // D^T
   }
 
   // loss = mean_t |b_t|^2 + reg ; rel = mean over nonzero targets of |b_t|/|G_t|
@@ -497,12 +494,17 @@ struct FitEngine {
     LSP_CUDA(cudaMemsetAsync(dgp.p, 0, pv.size() * 8, st));
     LSP_CUDA(cudaMemsetAsync(dgq.p, 0, qv.size() * 8, st));
     const double scale = 2.0 / T;
+    const size_t ddd = static_cast<size_t>(d) * d, nd = static_cast<size_t>(n) * d;
+    s0T.ensure(T * ddd * 8);
+    zt_all.ensure(T * nd * 8);
     for (int i = 0; i < T; ++i) {
-      chain(i);                                                     // S^T, Z^T, A1, V, D^T
+      double* sTp = s0T.as<double>() + i * ddd;
+      double* ztp = zt_all.as<double>() + i * nd;
+      chain(i, ztp, sTp);                                           // S^T, Z^T, A1, V, D^T
       launch_transpose(d, d, dT.p, d, dd.p, d, LSP_F64, st);        // D
       csc_gather(*Q, gT[i].as<double>(), m, xT.as<double>(), st);  // X^T = Q^T G^T (d x m)
       launch_transpose(d, m, xT.p, m, x.p, d, LSP_F64, st);         // X = G Q    (m x d)
-      csr_gather(*Q, sT.as<double>(), d, qs.as<double>(), st);      // Q S^T    (n x d)
+      csr_gather(*Q, sTp, d, qs.as<double>(), st);                  // Q S^T    (n x d)
       csc_gather(*Q, qs.as<double>(), d, a2T.as<double>(), st);     // A2^T = Gq S^T
       launch_transpose(d, d, a2T.p, d, a2.p, d, LSP_F64, st);       // A2 = S Gq
       csr_gather(*P, a2.as<double>(), d, w1.as<double>(), st);      // W1 = P A2 (m x d)
@@ -511,7 +513,7 @@ struct FitEngine {
           scale, dgp.as<double>());
       after_launch("sddmm_p");
       k_sddmm<<<egrid(static_cast<long long>(n) * 32), 256, 0, st>>>(
-          n, r, d, Q->pos.as<int>(), v.as<double>(), sT.as<double>(), zt.as<double>(), dT.as<double>(), d,
+          n, r, d, Q->pos.as<int>(), v.as<double>(), sTp, ztp, dT.as<double>(), d,
           scale, dgq.as<double>());
       after_launch("sddmm_q");
     }
