@@ -13,6 +13,7 @@
 //  stage 2  S^T[b][:] = sum_{j in CSC_Q(b)} q_jb Z^T[j][:]  -- coalesced row
 //           gathers of the L2-resident Z^T (k_gather).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "core.cuh"
@@ -628,11 +629,16 @@ void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t
     A.count = static_cast<int>(jobs.size());
     A.d = d;
     A.flag = flag;
+    // matrices in reverse order: stage 1 wrote the last matrices' Z^T most
+    // recently, so those reads are the likeliest L2 hits (LSP_STAGE2_REVERSE=0: forward)
+    const char* rev_env = std::getenv("LSP_STAGE2_REVERSE");
+    const bool rev = !(rev_env && rev_env[0] == '0');
     for (size_t i = 0; i < jobs.size(); ++i) {
-      const Projector& Q = *jobs[i].pr->q;
+      const size_t ji = rev ? jobs.size() - 1 - i : i;
+      const Projector& Q = *jobs[ji].pr->q;
       A.mat[i] = S2Mat{Q.csc_ptr.as<int>(), Q.csc_row.as<int>(), Q.csc_val.as<float>(),
-                       static_cast<const float*>(jobs[i].zt), jobs[i].pr->ldz(),
-                       static_cast<float*>(jobs[i].s_t)};
+                       static_cast<const float*>(jobs[ji].zt), jobs[ji].pr->ldz(),
+                       static_cast<float*>(jobs[ji].s_t)};
     }
     k_stage2_f4<<<dim3(d, A.count), kS2Threads, 0, st>>>(A);
     after_launch("stage2");
