@@ -86,6 +86,44 @@ __global__ void ring(const __grid_constant__ CUtensorMap map, const float* buf, 
   if (acc.x == 1234.5f) out[0] = acc.y + acc.z + acc.w;
 }
 
+// LDGSTS ring: each lane copies its 16 bytes of 4 rows per stage (cp.async.cg),
+// S stages per warp, then reads them back with LDS.128.
+__global__ void ldgsts(const float4* __restrict__ p, unsigned rows, int iters, int S, float* out) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* ring = sm + warp * S * 2048;
+  unsigned s = hash((blockIdx.x * (blockDim.x >> 5) + warp) * 7919u + 1);
+  auto issue = [&](int st) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      s = hash(s + k);
+      const float4* src = p + (size_t)(s % rows) * 32 + lane;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(ring + st * 2048 + k * 512 + lane * 16)),
+                   "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int st = 0; st < S; ++st) issue(st);
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int it = 0; it < iters; ++it) {
+    const int st = it % S;
+    // groups complete in order: wait until at most S-1 are pending
+    switch (S) {
+      case 2: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+      case 4: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+      case 6: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+      default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 v = *reinterpret_cast<const float4*>(ring + st * 2048 + k * 512 + lane * 16);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (it + S < iters) issue(st); else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  if (acc.x == 1234.5f) out[0] = acc.y + acc.z + acc.w;
+}
+
 template <int U>
 __global__ void ldg(const float4* __restrict__ p, unsigned rows, int iters, float* out) {
   const int lane = threadIdx.x & 31;
@@ -125,7 +163,7 @@ int main() {
     printf("%-40s %7.2f TB/s\n", name, bytes_moved / ms / 1e9);
   };
   const int iters = 4000;
-  for (int w : {8, 16, 32}) for (int S : {4, 8, 16}) {
+  for (int w : {16}) for (int S : {4}) {
     const int smem = w * S * (2048 + 8);
     if (smem > 227 * 1024) continue;
     char nm[64];
@@ -136,6 +174,15 @@ int main() {
     run(nm, [&] { ring<0><<<148, w * 32, smem>>>(map, p, rows, iters, S, out); }, mv);
     snprintf(nm, 64, "bulk x4 warps=%d stages=%d", w, S);
     run(nm, [&] { ring<1><<<148, w * 32, smem>>>(map, p, rows, iters, S, out); }, mv);
+  }
+  for (int w : {16, 24, 32}) for (int S : {2, 4, 6, 8}) {
+    const int smem = w * S * 2048;
+    if (smem > 227 * 1024) continue;
+    char nm[64];
+    CK(cudaFuncSetAttribute(ldgsts, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    snprintf(nm, 64, "ldgsts warps=%d stages=%d (%d KB)", w, S, smem / 1024);
+    run(nm, [&] { ldgsts<<<148, w * 32, smem>>>(reinterpret_cast<const float4*>(p), rows, iters, S, out); },
+        148.0 * w * iters * 2048.0);
   }
   for (int w : {16, 32}) {
     char nm[64];
