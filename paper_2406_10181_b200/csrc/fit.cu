@@ -18,6 +18,9 @@
 // (derivation in DESIGN.md).  Everything runs in fp64 on shadow fp64 copies of
 // the projectors; the fitted values are written back to the pair at the end.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -292,6 +295,7 @@ struct FitEngine {
   // batched loss intermediates
   DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, bqs, ba2T, ba2;
   DevBuf zt_all;  // per target Z^T = G^T P of the last gradient (reused by prepare_line)
+  DevBuf dgp, dgq;  // gradient accumulators (values layout)
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
   std::vector<double> gnorm2;
   DevBuf sT, s, u, a1, a1T, v, dT, dd, qs, a2T, a2, w1, x, xT, z, zt, zdt, parts, lparts;
@@ -488,7 +492,8 @@ struct FitEngine {
   void gradient(const std::vector<double>& pv, const std::vector<double>& qv,
                 const lsp_fit_config& cfg, std::vector<double>& gp, std::vector<double>& gq) {
     set_values(pv, qv);
-    DevBuf dgp, dgq;
+    // members: a cudaMalloc / cudaFree pair per call cost up to ~8 ms per GD step
+    // once the allocator had served earlier fits' multi-GB buffers
     dgp.ensure(std::max<size_t>(pv.size() * 8, 16));
     dgq.ensure(std::max<size_t>(qv.size() * 8, 16));
     LSP_CUDA(cudaMemsetAsync(dgp.p, 0, pv.size() * 8, st));
@@ -606,6 +611,12 @@ int lsp_fit(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_
     FitEngine fe(*pair, targets, t, ld, dtype, as_stream(stream));
     std::vector<double> pv = pair->p->h_val, qv = pair->q->h_val;
     const int budget = std::min(c.max_steps, c.timeout_steps);
+    const auto t_start = std::chrono::steady_clock::now();
+    int trials = 0;
+    const char* trace_env = std::getenv("LSP_FIT_TRACE");
+    const bool trace = trace_env && trace_env[0] == '1';
+    auto t_phase = t_start;
+    double t_grad = 0.0, t_prep = 0.0, t_trial = 0.0, t_other = 0.0;
     *report = lsp_fit_report{};
     int ncurve = 0;
     auto push = [&](double l) {
@@ -619,15 +630,27 @@ int lsp_fit(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_
     bool success = rel <= c.alpha, stalled = false;
     std::vector<double> gp, gq, tp(pv.size()), tq(qv.size());
     for (int step = 0; step < budget && !success; ++step) {
+      auto tick = [&](double& acc) {  // LSP_FIT_TRACE phase timing (synchronises)
+        if (!trace) return;
+        LSP_CUDA(cudaStreamSynchronize(fe.st));
+        const auto now = std::chrono::steady_clock::now();
+        acc += std::chrono::duration<double>(now - t_phase).count();
+        t_phase = now;
+      };
+      tick(t_other);
       fe.gradient(pv, qv, c, gp, gq);
+      tick(t_grad);
       fe.prepare_line(pv, qv, gp, gq);
+      tick(t_prep);
       double trial_step = c.step_size;
       bool accepted = false;
       for (int halving = 0; halving < 40; ++halving) {
+        ++trials;
         for (size_t i = 0; i < pv.size(); ++i) tp[i] = pv[i] - trial_step * gp[i];
         for (size_t i = 0; i < qv.size(); ++i) tq[i] = qv[i] - trial_step * gq[i];
         double tl = 0.0, trel = 0.0;
         fe.loss(tp, tq, c, &tl, &trel, trial_step);
+        tick(t_trial);
         if (std::isfinite(tl) && tl < loss) {
           pv.swap(tp);
           qv.swap(tq);
@@ -646,6 +669,13 @@ int lsp_fit(lsp_pair_t pair, const void* const* targets, int t, int64_t ld, lsp_
       push(loss);
       success = rel <= c.alpha;
     }
+    if (trace)
+      std::fprintf(stderr,
+                   "lsp_fit: %d x %d, T=%d: %d steps, %d loss evaluations, %.3f s (gradient %.3f, "
+                   "line prep %.3f, trials %.3f, other %.3f)\n",
+                   fe.m, fe.n, t, report->steps, trials + 1,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(), t_grad,
+                   t_prep, t_trial, t_other);
     report->final_rel_bias = rel;
     report->success = success ? 1 : 0;
     report->stalled = stalled ? 1 : 0;

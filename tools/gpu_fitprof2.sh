@@ -1,7 +1,7 @@
 # Launch list of a capped device fit (C3 MLP shape, T targets): per-kernel totals and
 # per-launch duration classes of the fp64 gather.
 mkdir -p gpurun_out
-bash tools/gpu_fitprof.sh ${1:-2}
+bash tools/gpu_fitprof.sh ${1:-2} ${2:-2048} ${3:-5504}
 python - <<'PY'
 import csv, re, collections
 rows=[l for l in open('gpurun_out/fit_launches.csv') if l.startswith('"')]
