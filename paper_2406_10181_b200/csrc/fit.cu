@@ -171,56 +171,81 @@ __global__ void k_gram(int da, int db, int rb, const int* __restrict__ a_csc_ptr
 }
 
 // fp64 GEMM C = A (MxK) * B (KxN), row-major, on the FP64 tensor cores
-// (mma.sync m8n8k4 f64): 64 x 64 block tiles, K staged 16 at a time through
-// shared memory, 8 warps of 16 x 32 (2 x 4 MMA tiles of 8 x 8).  Used only by
-// reproject_state's d^3 transfer products (the one dense
-// contraction on the path); zero-filled edges handle any M, N, K.
-constexpr int kMT = 64, kNT = 64, kKT = 16;
+// (mma.sync m8n8k4 f64 -> DMMA): 128 x 64 block tiles, K staged 16 at a time
+// through shared memory with the next slice prefetched into registers, 8 warps of 32 x 32 (4 x 4 MMA tiles of
+// 8 x 8: 8 fragment loads per 16 MMAs).  Used only by reproject_state's d^3
+// transfer products (the one dense contraction on the path);
+// zero-filled edges handle any M, N, K.
+constexpr int kMT = 128, kNT = 64, kKT = 16;
 __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double* __restrict__ A,
                                                const double* __restrict__ B, double* __restrict__ C) {
   __shared__ double As[kMT][kKT + 1];
   __shared__ double Bs[kKT][kNT + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps, warp tile 16 x 32
+  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps, warp tile 32 x 32
   const int row0 = blockIdx.y * kMT, col0 = blockIdx.x * kNT;
   const int g = lane >> 2, q = lane & 3;
-  double acc[2][4][2];
+  double acc[4][4][2];
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  double ra[kMT * kKT / 256], rb[kKT * kNT / 256];  // next K slice, in registers
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < kMT * kKT / 256; ++i) {
+      const int t = tid + 256 * i, r = t / kKT, c = t % kKT;
+      ra[i] = (row0 + r < M && k0 + c < K) ? A[static_cast<long long>(row0 + r) * K + k0 + c] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kKT * kNT / 256; ++i) {
+      const int t = tid + 256 * i, r = t / kNT, c = t % kNT;
+      rb[i] = (k0 + r < K && col0 + c < N) ? B[static_cast<long long>(k0 + r) * N + col0 + c] : 0.0;
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int i = 0; i < kMT * kKT / 256; ++i) {
+      const int t = tid + 256 * i;
+      As[t / kKT][t % kKT] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < kKT * kNT / 256; ++i) {
+      const int t = tid + 256 * i;
+      Bs[t / kNT][t % kNT] = rb[i];
+    }
+  };
+  fetch(0);
+  stash();
+  __syncthreads();
   for (int k0 = 0; k0 < K; k0 += kKT) {
-    for (int t = tid; t < kMT * kKT; t += 256) {
-      const int r = t / kKT, c = t % kKT;
-      As[r][c] = (row0 + r < M && k0 + c < K) ? A[static_cast<long long>(row0 + r) * K + k0 + c] : 0.0;
-    }
-    for (int t = tid; t < kKT * kNT; t += 256) {
-      const int r = t / kNT, c = t % kNT;
-      Bs[r][c] = (k0 + r < K && col0 + c < N) ? B[static_cast<long long>(k0 + r) * N + col0 + c] : 0.0;
-    }
-    __syncthreads();
+    if (k0 + kKT < K) fetch(k0 + kKT);  // global loads of the next slice overlap the MMAs
 #pragma unroll
     for (int kk = 0; kk < kKT; kk += 4) {
-      double a[2], b[4];
+      double a[4], b[4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) a[mt] = As[wm * 16 + mt * 8 + g][kk + q];   // A: row g, k q
+      for (int mt = 0; mt < 4; ++mt) a[mt] = As[wm * 32 + mt * 8 + g][kk + q];   // A: row g, k q
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) b[nt] = Bs[kk + q][wn * 32 + nt * 8 + g];   // B: k q, col g
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
           asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
               : "=d"(acc[mt][nt][0]), "=d"(acc[mt][nt][1])
               : "d"(a[mt]), "d"(b[nt]), "d"(acc[mt][nt][0]), "d"(acc[mt][nt][1]));
     }
-    __syncthreads();
+    __syncthreads();  // the slice is consumed
+    if (k0 + kKT < K) {
+      stash();
+      __syncthreads();
+    }
   }
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
-      const int r = row0 + wm * 16 + mt * 8 + g, c = col0 + wn * 32 + nt * 8 + 2 * q;  // D: row g, cols 2q, 2q+1
+      const int r = row0 + wm * 32 + mt * 8 + g, c = col0 + wn * 32 + nt * 8 + 2 * q;  // D: row g, cols 2q, 2q+1
       if (r < M && c < N) C[static_cast<long long>(r) * N + c] = acc[mt][nt][0];
       if (r < M && c + 1 < N) C[static_cast<long long>(r) * N + c + 1] = acc[mt][nt][1];
     }
