@@ -9,7 +9,11 @@
  * ranks wait for it (any out-of-band channel works; torch users ship it with
  * torch.distributed, paper_2406_10181_b200.Comm.from_group).
  *
- *   ./dp_layer_step RANK NRANKS ID_FILE [STEPS]
+ *   ./dp_layer_step RANK NRANKS ID_FILE [STEPS] [sched]
+ *
+ * With "sched" the steps go through the library's native schedule instead
+ * (lsp_schedule_step: compress, the all-reduce on its comm stream, Adam and
+ * apply, all enqueued by the library); the checksum is the same.
  *
  * Prints one line per rank: a checksum of W after the steps.  All ranks use
  * the same W and projectors and rank-dependent gradients, so every rank must
@@ -50,12 +54,13 @@ static float urand(unsigned long long* s) { /* xorshift, [-1, 1) */
 
 int main(int argc, char** argv) {
   if (argc < 4) {
-    fprintf(stderr, "usage: %s RANK NRANKS ID_FILE [STEPS]\n", argv[0]);
+    fprintf(stderr, "usage: %s RANK NRANKS ID_FILE [STEPS] [sched]\n", argv[0]);
     return 2;
   }
   const int rank = atoi(argv[1]), nranks = atoi(argv[2]);
   const char* id_file = argv[3];
   const int steps = argc > 4 ? atoi(argv[4]) : 3;
+  const int use_sched = argc > 5 && strcmp(argv[5], "sched") == 0;
   enum { NMAT = 3, D = 64, R = 4 };
   const int shape[NMAT][2] = {{256, 256}, {256, 704}, {704, 256}};
   CU(cudaSetDevice(0));
@@ -111,11 +116,18 @@ int main(int argc, char** argv) {
     CK(lsp_layer_bind(layer, i, g[i], shape[i][1], LSP_F32, w[i], shape[i][1], LSP_F32));
   cudaStream_t st;
   CU(cudaStreamCreate(&st));
+  lsp_schedule_t sched = NULL;
+  if (use_sched) CK(lsp_schedule_create(1, &layer, comm, &sched));
   for (int s = 0; s < steps; ++s) {
-    CK(lsp_layer_compress(layer, st));
-    CK(lsp_layer_allreduce(layer, comm, st));
-    CK(lsp_layer_update(layer, 1e-3, 0, st));
+    if (sched) {
+      CK(lsp_schedule_step(sched, 1e-3, st));
+    } else {
+      CK(lsp_layer_compress(layer, st));
+      CK(lsp_layer_allreduce(layer, comm, st));
+      CK(lsp_layer_update(layer, 1e-3, 0, st));
+    }
   }
+  if (sched) CK(lsp_schedule_destroy(sched));
   CK(lsp_layer_check(layer, st)); /* NumericError on every rank if any S was non-finite */
   double sum = 0.0;
   for (int i = 0; i < NMAT; ++i) {

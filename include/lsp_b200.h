@@ -299,6 +299,28 @@ int lsp_allreduce_mean(lsp_comm_t comm, void* buf, int64_t count, lsp_dtype dtyp
 int lsp_layer_allreduce(lsp_layer_t layer, lsp_comm_t comm, lsp_stream_t stream);
 
 /* ----------------------------------------------------------------------------
+ * Multi-layer step schedule (SURVEY 8(b) lsp_schedule_*): the layer-wise
+ * pipeline the reference only models (build_lsp_layerwise,
+ * proj/src/schedule_sim.cpp:255-283) in place of its sequential per-layer loop
+ * (proj/src/trainer.cpp:186-198).  One step, layers in backward order:
+ * [backward(l) on the caller's stream] -> compress(l) -> all-reduce(S_l) on a
+ * comm stream (when comm != NULL) -> Adam + apply of layer l+1, with the
+ * all-reduce of layer l overlapping the compress of layer l-1.  With a
+ * backward callback the LSP work runs on the schedule's own stream, compress(l)
+ * gated by an event recorded after backward(l), and the caller's stream joins
+ * it at the end.  Side streams are forked from and joined into `stream` by
+ * events, so a step can be captured in a CUDA graph.
+ * -------------------------------------------------------------------------- */
+typedef struct lsp_schedule_s* lsp_schedule_t;
+/* Enqueue the backward of layer `layer` (producing its bound gradients) on `stream`. */
+typedef void (*lsp_backward_fn)(int layer, lsp_stream_t stream, void* user);
+/* layers in forward order; comm may be NULL (single rank, no exchange). */
+int lsp_schedule_create(int count, const lsp_layer_t* layers, lsp_comm_t comm, lsp_schedule_t* out);
+int lsp_schedule_set_backward(lsp_schedule_t sched, lsp_backward_fn fn, void* user);
+int lsp_schedule_step(lsp_schedule_t sched, double lr, lsp_stream_t stream);
+int lsp_schedule_destroy(lsp_schedule_t sched);
+
+/* ----------------------------------------------------------------------------
  * Projector fit (proj/src/projector.cpp:189-315), on the device in fp64.
  * targets: T device pointers to m x n matrices (ld, dtype shared).
  * -------------------------------------------------------------------------- */

@@ -34,6 +34,7 @@ from .projector import (  # noqa: F401
     FitConfig,
     FitReport,
     Layer,
+    Schedule,
     derive_seed,
     identity_pattern,
     init_sparse,
@@ -49,7 +50,7 @@ from .projector import (  # noqa: F401
 )
 
 __all__ = [
-    "AdamState", "Comm", "nccl_version", "NcclError", "DevicePair", "Layer", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
+    "AdamState", "Comm", "nccl_version", "NcclError", "DevicePair", "Layer", "Schedule", "DeviceProjector", "FitConfig", "FitReport", "derive_seed",
     "identity_pattern", "init_sparse", "load_projector", "projector_gram", "reproject_state", "maybe_update",
     "save_projector", "step", "subsample_size", "update", "LspError", "InvalidArgument",
     "NumericError", "IoError", "CudaError", "Layout", "lib", "library_path", "launch_count", "set_sm_budget",

@@ -143,6 +143,10 @@ _SIGS = {
     "lsp_allreduce_mean": (_i, [_vp, _vp, _i64, _i, _vp]),
     "lsp_layer_allreduce": (_i, [_vp, _vp, _vp]),
     "lsp_reproject_state": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "lsp_schedule_create": (_i, [_i, C.POINTER(_vp), _vp, C.POINTER(_vp)]),
+    "lsp_schedule_set_backward": (_i, [_vp, _vp, _vp]),
+    "lsp_schedule_step": (_i, [_vp, _d, _vp]),
+    "lsp_schedule_destroy": (_i, [_vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -652,6 +652,59 @@ class Comm:
             pass
 
 
+# void (*)(int layer, cudaStream_t stream, void* user)
+_BACKWARD_FN = C.CFUNCTYPE(None, C.c_int, C.c_void_p, C.c_void_p)
+
+
+class Schedule:
+    """Native multi-layer step schedule (include/lsp_b200.h lsp_schedule_*): the
+    same pipeline as ``schedule.LayerSchedule`` -- layers in backward order,
+    compress(l) -> all-reduce(S_l) on a comm stream -> Adam + apply of layer l+1,
+    optionally gated per layer by a backward producer -- enqueued by the
+    library in C++ (csrc/schedule.cpp).  Capturable in a CUDA graph.
+
+    backward(layer, stream): optional; called on the host in backward order to
+    enqueue the backward of ``layer`` on ``stream`` (a torch.cuda.ExternalStream).
+    """
+
+    def __init__(self, layers: Sequence[Layer], comm: Optional[Comm] = None, backward=None):
+        self.layers = list(layers)
+        self.comm = comm
+        arr = (C.c_void_p * len(self.layers))(*[l.handle for l in self.layers])
+        h = C.c_void_p()
+        lib.schedule_create(len(self.layers), arr, comm.handle if comm is not None else None,
+                            C.byref(h))
+        self._h = h
+        self._cb = None
+        if backward is not None:
+            self.set_backward(backward)
+
+    def set_backward(self, backward):
+        torch = _torch()
+
+        def tramp(layer, stream_ptr, _user):
+            # NULL (ctypes None) is the legacy default stream
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr or 0)):
+                backward(int(layer), torch.cuda.current_stream())
+
+        self._cb = _BACKWARD_FN(tramp) if backward is not None else None
+        lib.schedule_set_backward(self._h, self._cb, None)
+
+    def step(self, lr: float, stream=None):
+        lib.schedule_step(self._h, float(lr), _stream(stream))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.schedule_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def nccl_version() -> int:
     v = C.c_int()
     lib.nccl_version(C.byref(v))

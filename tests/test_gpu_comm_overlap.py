@@ -168,6 +168,11 @@ def test_c_dp_example_runs(cuda, tmp_path):
                          text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert "rank 0/1 steps 3 checksum" in out.stdout
+    # the same steps through the native schedule (lsp_schedule_step): same checksum
+    out2 = subprocess.run([exe, "0", "1", str(tmp_path / "id2.bin"), "3", "sched"],
+                          capture_output=True, text=True, timeout=120)
+    assert out2.returncode == 0, out2.stderr
+    assert out2.stdout == out.stdout
 
 
 def test_schedule_comm_graph_capture(comm):
@@ -193,3 +198,69 @@ def test_schedule_comm_graph_capture(comm):
     torch.cuda.synchronize()
     for x, y in zip(wa, wb):
         assert torch.equal(x, y)
+
+
+# ---- the native schedule (csrc/schedule.cpp, lsp_schedule_*) -----------------
+@pytest.mark.parametrize("mode", ["plain", "comm", "backward", "backward+comm"])
+def test_native_schedule_matches_python(cuda, comm, mode):
+    """lsp_schedule_step (C++) enqueues exactly LayerSchedule's pipeline: weights
+    and moments bitwise equal after several steps, in every mode."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    use_comm = "comm" in mode
+    use_bwd = mode.startswith("backward")
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    if not use_bwd:
+        for li in range(L):
+            _backward(aa)(li)
+            _backward(ab)(li)
+    sa = LayerSchedule(la, 1e-3, comm=comm if use_comm else None,
+                       backward=_backward(aa) if use_bwd else None)
+    bwd_b = _backward(ab)
+    order = []
+
+    def native_bwd(li, stream):
+        order.append(li)
+        bwd_b(li)
+
+    sb = lsp.Schedule(lb, comm=comm if use_comm else None, backward=native_bwd if use_bwd else None)
+    for _ in range(3):
+        sa.step()
+        sb.step(1e-3)
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+    for lx, ly in zip(la, lb):
+        for i in range(len(SHAPES)):
+            mx, vx, tx = lx.adam_get(i)
+            my, vy, ty = ly.adam_get(i)
+            assert tx == ty and (mx == my).all() and (vx == vy).all()
+    if use_bwd:
+        assert order[:L] == list(reversed(range(L)))  # backward order per step
+
+
+def test_native_schedule_graph_capture(cuda, comm):
+    """The native step (comm stream fork/join and the backward producer's stream
+    events) captures into one CUDA graph; replays equal eager native steps."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    la, wa, aa = _build()
+    sa = lsp.Schedule(la, comm=comm, backward=lambda li, s: _backward(aa)(li))
+    for _ in range(4):
+        sa.step(1e-3)
+    lb, wb, ab = _build()
+    sb = lsp.Schedule(lb, comm=comm, backward=lambda li, s: _backward(ab)(li))
+    sb.step(1e-3)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sb.step(1e-3)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+
+
+def test_native_schedule_rejects_bad_input(cuda):
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.Schedule([])
