@@ -77,6 +77,10 @@ def parse():
                     help="1 (default): capture one step in a CUDA graph and replay it in the "
                          "timed region (N=1 only; the per-phase split comes from one eager "
                          "step just before); 0: eager launches")
+    ap.add_argument("--schedule", choices=("native", "python"), default="native",
+                    help="step driver of the timed region: the library's C++ schedule "
+                         "(lsp_schedule_step, default) or schedule.LayerSchedule (Python); "
+                         "the per-phase split always uses LayerSchedule's hooks")
     ap.add_argument("--concurrent", type=int, default=0,
                     help="1: compress and update chains on two streams (schedule.py)")
     ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
@@ -435,10 +439,16 @@ def run_ours(args):
     # the id and runs the barriers / max-over-ranks timing)
     comm = lsp.Comm.from_group() if world > 1 else None
     sched = LayerSchedule(layers, args.lr, comm=comm, record=record, streams=streams)
+    native = None
+    if args.schedule == "native" and streams is None:
+        native = lsp.Schedule(layers, comm=comm)  # csrc/schedule.cpp, same pipeline
 
     def one_step(record=False):
         recording[0] = record
-        sched.step()
+        if native is not None and not record:
+            native.step(args.lr)
+        else:
+            sched.step()
         recording[0] = False
 
     for _ in range(args.warmup):
@@ -451,7 +461,7 @@ def run_ours(args):
         graph = torch.cuda.CUDAGraph()
         g0 = lsp.launch_count()
         with torch.cuda.graph(graph):
-            sched.step()
+            one_step()
         graph_launches = lsp.launch_count() - g0
         graph.replay()  # warm the graph once
         torch.cuda.synchronize()
@@ -526,11 +536,13 @@ def run_ours(args):
                                   if graph is not None else False),
                    "streams": ("2 (compress | update, SM budget %d | %d)"
                                % (args.sms_compress, args.sms_update)) if args.concurrent else "1",
+                   "schedule": ("native (lsp_schedule_step, csrc/schedule.cpp)" if native is not None
+                                else "python (schedule.LayerSchedule)"),
                    "step_hbm_bytes_alg": balg,
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},
         "roofline": {"kernel": "k_apply_y (grouped streaming decompress-and-apply W -= lr P Y, "
-                               "1 launch per layer; Y = delta Q^T built by k_build_y_vec just "
+                               "1 launch per layer; Y = delta Q^T built by k_build_y_tile just "
                                "before, timed separately as build_ms)",
                      "bound": "hbm", "achieved": app_ach, "peak": peak, "unit": "GB/s",
                      "frac": app_ach / peak, "traffic": traffic,
