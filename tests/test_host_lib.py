@@ -108,3 +108,19 @@ def test_device_calls_fail_loudly_without_gpu():
     pos, val = lsp.init_sparse(8, 4, 2, 1)
     with pytest.raises(lsp.CudaError):
         lsp.DeviceProjector(8, 4, 2, pos, val)
+
+
+def test_schedule_rejects_bad_args():
+    """lsp_schedule_create validates its arguments before touching the device
+    (InvalidArgument, like the reference's std::invalid_argument)."""
+    import ctypes as C
+
+    h = C.c_void_p()
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.schedule_create(0, None, None, C.byref(h))
+    arr = (C.c_void_p * 2)(None, None)
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.schedule_create(2, arr, None, C.byref(h))
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.schedule_step(None, 1e-3, None)
+    lsp.lib.schedule_destroy(None)  # a null handle is a no-op
