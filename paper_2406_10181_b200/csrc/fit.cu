@@ -113,39 +113,76 @@ __global__ void k_sddmm(int R, int k, int d, const int* __restrict__ pos,
   }
 }
 
-// Deterministic per-block partials of <a, b> and <c, e> over `cnt` elements
-// (partials[block] and partials[gridDim.x + block]).
-// Batched over blockIdx.y: operands at + y*cnt, partials at + y*2*gridDim.x.
-__global__ void k_dot2(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
-                       const double* __restrict__ c, const double* __restrict__ e,
-                       double* __restrict__ partials) {
-  const long long off = static_cast<long long>(blockIdx.y) * cnt;
-  a += off, b += off, c += off, e += off;
-  partials += static_cast<long long>(blockIdx.y) * 2 * gridDim.x;
-  double s = 0.0, t = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x) {
-    s = fma(a[i], b[i], s);
-    t = fma(c[i], e[i], t);
+// Fused trial prologue, one 32 x 32 tile per block, gridDim.z = target:
+//   S^T(t) = s0 - t s1 + t^2 s2 (s1 == nullptr: S^T = s0 as given, not rewritten)
+// written to sT, its transpose to s, and per-block partial sums of |S|^2 in
+// fixed order (partials[z][block]).  Replaces a separate polynomial, transpose
+// and dot-product pass.
+__global__ void k_poly_tile(int d, long long dd, const double* s0, const double* __restrict__ s1,
+                            const double* __restrict__ s2, double t, double* sT,
+                            double* __restrict__ s, double* __restrict__ partials) {  // s0 may alias sT
+  __shared__ double tile[32][33];
+  __shared__ double red[256];
+  const long long off = static_cast<long long>(blockIdx.z) * dd;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // column / row of S^T
+  double ss = 0.0;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = by + y, c = bx + threadIdx.x;
+    double v = 0.0;
+    if (r < d && c < d) {
+      const long long i = off + static_cast<long long>(r) * d + c;
+      if (s1) {
+        v = fma(t * t, s2[i], fma(-t, s1[i], s0[i]));
+        sT[i] = v;
+      } else {
+        v = s0[i];
+      }
+      ss = fma(v, v, ss);
+    }
+    tile[y][threadIdx.x] = v;
   }
-  __shared__ double red[2][256];
-  red[0][threadIdx.x] = s;
-  red[1][threadIdx.x] = t;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double x = 0.0, y = 0.0;
-    for (int i = 0; i < 256; ++i) x += red[0][i], y += red[1][i];
-    partials[blockIdx.x] = x;
-    partials[gridDim.x + blockIdx.x] = y;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = bx + y, c = by + threadIdx.x;  // S[r][c] = S^T[c][r]
+    if (r < d && c < d) s[off + static_cast<long long>(r) * d + c] = tile[threadIdx.x][y];
+  }
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  red[tid] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    double x = 0.0;
+    for (int i = 0; i < 256; ++i) x += red[i];
+    partials[static_cast<long long>(blockIdx.z) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = x;
   }
 }
 
-// out = a - t*b + t^2*c  (S^T along the line-search ray, see FitEngine::prepare_line)
-__global__ void k_poly2(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
-                        const double* __restrict__ c, double t, double* __restrict__ out) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x)
-    out[i] = fma(t * t, c[i], fma(-t, b[i], a[i]));
+// <A1, A2> with A2 given as A2^T (row-major), one 32 x 32 tile per block
+// (A2^T tile staged transposed through shared memory), gridDim.z = target;
+// per-block partials in fixed order.  Replaces the A2 transpose + dot pass.
+__global__ void k_dot_tile(int d, long long dd, const double* __restrict__ a1,
+                           const double* __restrict__ a2t, double* __restrict__ partials) {
+  __shared__ double tile[32][33];
+  __shared__ double red[256];
+  const long long off = static_cast<long long>(blockIdx.z) * dd;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // A1 tile: rows by.., cols bx..
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = bx + y, c = by + threadIdx.x;  // A2^T[r][c] = A2[c][r]
+    tile[y][threadIdx.x] = (r < d && c < d) ? a2t[off + static_cast<long long>(r) * d + c] : 0.0;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = by + y, c = bx + threadIdx.x;  // A1[r][c] * A2[r][c], A2[r][c] = tile[c-bx][r-by]
+    if (r < d && c < d) acc = fma(a1[off + static_cast<long long>(r) * d + c], tile[threadIdx.x][y], acc);
+  }
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  red[tid] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double x = 0.0;
+    for (int i = 0; i < 256; ++i) x += red[i];
+    partials[static_cast<long long>(blockIdx.z) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = x;
+  }
 }
 
 // out (da x db, row-major) = A^T B for two projectors over the same rows, in
@@ -334,7 +371,7 @@ struct FitEngine {
   std::unique_ptr<lsp_projector_s> P, Q, Pd, Qd;  // Pd, Qd: the descent direction's values
   // per target (contiguous, target-major): S^T(t) = s0T - t s1T + t^2 s2T, and the
   // batched loss intermediates
-  DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, bqs, ba2T, ba2;
+  DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, bqs, ba2T;
   DevBuf zt_all;  // per target Z^T = G^T P of the last gradient (reused by prepare_line)
   DevBuf dgp, dgq;  // gradient accumulators (values layout)
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
@@ -442,48 +479,52 @@ struct FitEngine {
                     LSP_F64, 1.0, 0.0, nullptr, nullptr, st);
   }
 
-  void bias2_from_bsT() {
+  void bias2_from_bsT(double line_t) {
     const size_t dd = static_cast<size_t>(d) * d, md = static_cast<size_t>(m) * d,
                  nd = static_cast<size_t>(n) * d;
-    bs.ensure(T * dd * 8), ba1.ensure(T * dd * 8), ba2T.ensure(T * dd * 8), ba2.ensure(T * dd * 8);
+    bs.ensure(T * dd * 8), ba1.ensure(T * dd * 8), ba2T.ensure(T * dd * 8);
     bu.ensure(T * md * 8), bqs.ensure(T * nd * 8);
+    const int tiles = ceil_div(d, 32);
+    const size_t np = static_cast<size_t>(tiles) * tiles;
+    lparts.ensure(T * 2 * np * sizeof(double));
+    double* ss_parts = lparts.as<double>();
+    double* ag_parts = lparts.as<double>() + T * np;
+    const dim3 tg(tiles, tiles, T), tb(32, 8);
+    // S^T (polynomial, or as compressed), its transpose S and |S|^2
+    k_poly_tile<<<tg, tb, 0, st>>>(d, static_cast<long long>(dd), line_t >= 0.0 ? s0T.as<double>() : bsT.as<double>(),
+                                   line_t >= 0.0 ? s1T.as<double>() : nullptr,
+                                   line_t >= 0.0 ? s2T.as<double>() : nullptr, line_t, bsT.as<double>(),
+                                   bs.as<double>(), ss_parts);
+    after_launch("poly_tile");
     const double* sTp = bsT.as<double>();
-    launch_transpose_batch(d, d, sTp, d, dd, bs.as<double>(), d, dd, T, st);              // S
     gather_batch(*P, true, bs.as<double>(), dd, bu.as<double>(), md);      // U    = P S
     gather_batch(*P, false, bu.as<double>(), md, ba1.as<double>(), dd);    // A1   = Gp S
     gather_batch(*Q, true, sTp, dd, bqs.as<double>(), nd);                 // Q S^T
     gather_batch(*Q, false, bqs.as<double>(), nd, ba2T.as<double>(), dd);  // A2^T = Gq S^T
-    launch_transpose_batch(d, d, ba2T.as<double>(), d, dd, ba2.as<double>(), d, dd, T, st);  // A2 = S Gq
-    k_dot2<<<dim3(kRedBlocks, T), 256, 0, st>>>(static_cast<long long>(dd), ba1.as<double>(), ba2.as<double>(),
-                                                sTp, sTp, lparts.as<double>());
-    after_launch("dot2");
+    k_dot_tile<<<tg, tb, 0, st>>>(d, static_cast<long long>(dd), ba1.as<double>(), ba2T.as<double>(), ag_parts);
+    after_launch("dot_tile");
   }
 
   // all targets' |b_i|^2 with one synchronisation (clamped at 0: the identity
   // can round below zero for an exactly representable target); line_t >= 0:
   // S^T from the prepared line-search polynomial instead of a pass over G
   std::vector<double> bias2_all(double line_t = -1.0) {
-    lparts.ensure(static_cast<size_t>(T) * 2 * kRedBlocks * sizeof(double));
     const size_t dd = static_cast<size_t>(d) * d;
     bsT.ensure(T * dd * 8);
-    if (line_t >= 0.0) {
-      const long long cnt = static_cast<long long>(T * dd);
-      k_poly2<<<egrid(cnt), 256, 0, st>>>(cnt, s0T.as<double>(), s1T.as<double>(), s2T.as<double>(), line_t,
-                                          bsT.as<double>());
-      after_launch("poly2");
-    } else {
+    if (line_t < 0.0)
       for (int i = 0; i < T; ++i) compress(i, zt.as<double>(), bsT.as<double>() + i * dd);
-    }
-    bias2_from_bsT();
-    std::vector<double> h(static_cast<size_t>(T) * 2 * kRedBlocks);
+    bias2_from_bsT(line_t);
+    const int tiles = ceil_div(d, 32);
+    const size_t np = static_cast<size_t>(tiles) * tiles;
+    std::vector<double> h(T * 2 * np);
     LSP_CUDA(cudaMemcpyAsync(h.data(), lparts.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     LSP_CUDA(cudaStreamSynchronize(st));
     std::vector<double> out(T);
     for (int i = 0; i < T; ++i) {
-      double ag = 0.0, ss = 0.0;
-      for (int b = 0; b < kRedBlocks; ++b) {
-        ag += h[static_cast<size_t>(i) * 2 * kRedBlocks + b];
-        ss += h[static_cast<size_t>(i) * 2 * kRedBlocks + kRedBlocks + b];
+      double ss = 0.0, ag = 0.0;
+      for (size_t b = 0; b < np; ++b) {
+        ss += h[i * np + b];
+        ag += h[T * np + i * np + b];
       }
       out[i] = std::max(0.0, gnorm2[i] - 2.0 * ss + ag);
     }
