@@ -208,18 +208,19 @@ __global__ void k_gram(int da, int db, int rb, const int* __restrict__ a_csc_ptr
 }
 
 // fp64 GEMM C = A (MxK) * B (KxN), row-major, on the FP64 tensor cores
-// (mma.sync m8n8k4 f64 -> DMMA): 128 x 64 block tiles, K staged 16 at a time
-// through shared memory with the next slice prefetched into registers, 8 warps of 32 x 32 (4 x 4 MMA tiles of
-// 8 x 8: 8 fragment loads per 16 MMAs).  Used only by reproject_state's d^3
+// (mma.sync m8n8k4 f64 -> DMMA): 64 x 64 block tiles (256 CTAs at d = 1024),
+// K staged 16 at a time through shared memory with the next slice prefetched
+// into registers, 4 warps of 32 x 32 (4 x 4 MMA tiles of 8 x 8: 8 fragment
+// loads per 16 MMAs).  Used only by reproject_state's d^3
 // transfer products (the one dense contraction on the path);
 // zero-filled edges handle any M, N, K.
-constexpr int kMT = 128, kNT = 64, kKT = 16;
-__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double* __restrict__ A,
+constexpr int kMT = 64, kNT = 64, kKT = 16, kGW = 4;  // 4 warps of 32 x 32
+__global__ void __launch_bounds__(kGW * 32) k_dgemm(int M, int N, int K, const double* __restrict__ A,
                                                const double* __restrict__ B, double* __restrict__ C) {
   __shared__ double As[kMT][kKT + 1];
   __shared__ double Bs[kKT][kNT + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps, warp tile 32 x 32
+  const int wm = warp >> 1, wn = warp & 1;  // 2 x 2 warps, warp tile 32 x 32
   const int row0 = blockIdx.y * kMT, col0 = blockIdx.x * kNT;
   const int g = lane >> 2, q = lane & 3;
   double acc[4][4][2];
@@ -227,28 +228,28 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-  double ra[kMT * kKT / 256], rb[kKT * kNT / 256];  // next K slice, in registers
+  double ra[kMT * kKT / (kGW * 32)], rb[kKT * kNT / (kGW * 32)];  // next K slice, in registers
   auto fetch = [&](int k0) {
 #pragma unroll
-    for (int i = 0; i < kMT * kKT / 256; ++i) {
-      const int t = tid + 256 * i, r = t / kKT, c = t % kKT;
+    for (int i = 0; i < kMT * kKT / (kGW * 32); ++i) {
+      const int t = tid + kGW * 32 * i, r = t / kKT, c = t % kKT;
       ra[i] = (row0 + r < M && k0 + c < K) ? A[static_cast<long long>(row0 + r) * K + k0 + c] : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < kKT * kNT / 256; ++i) {
-      const int t = tid + 256 * i, r = t / kNT, c = t % kNT;
+    for (int i = 0; i < kKT * kNT / (kGW * 32); ++i) {
+      const int t = tid + kGW * 32 * i, r = t / kNT, c = t % kNT;
       rb[i] = (k0 + r < K && col0 + c < N) ? B[static_cast<long long>(k0 + r) * N + col0 + c] : 0.0;
     }
   };
   auto stash = [&]() {
 #pragma unroll
-    for (int i = 0; i < kMT * kKT / 256; ++i) {
-      const int t = tid + 256 * i;
+    for (int i = 0; i < kMT * kKT / (kGW * 32); ++i) {
+      const int t = tid + kGW * 32 * i;
       As[t / kKT][t % kKT] = ra[i];
     }
 #pragma unroll
-    for (int i = 0; i < kKT * kNT / 256; ++i) {
-      const int t = tid + 256 * i;
+    for (int i = 0; i < kKT * kNT / (kGW * 32); ++i) {
+      const int t = tid + kGW * 32 * i;
       Bs[t / kNT][t % kNT] = rb[i];
     }
   };
@@ -315,7 +316,7 @@ double dot_sync(const double* a, const double* b, long long cnt, DevBuf& parts, 
 
 void dgemm(int M, int N, int K, const double* A, const double* B, double* C, cudaStream_t st) {
   dim3 grid(ceil_div(N, kNT), ceil_div(M, kMT));
-  k_dgemm<<<grid, 256, 0, st>>>(M, N, K, A, B, C);
+  k_dgemm<<<grid, kGW * 32, 0, st>>>(M, N, K, A, B, C);
   after_launch("dgemm");
 }
 
