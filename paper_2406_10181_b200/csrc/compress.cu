@@ -353,17 +353,19 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
 }
 
 // fp64 fast form (no partials; c, lds, ldo, ldi even; 16-byte aligned rows):
-// one warp per (column pass of 256 doubles, output row), passes outermost so
+// one warp per (column pass of 128 doubles, output row), passes outermost so
 // the warps in flight cover every row for a few column passes (the source
 // rows of those columns come from HBM once, then L2).  Lane = 2 adjacent
 // columns per 64-column chunk (16-byte loads, 512 bytes per warp
-// instruction); entries in groups of 4 with all 16 loads of a group in flight.
+// instruction); entries in groups of 4 with all 8 loads of a group in flight,
+// 64 registers so four 8-warp blocks share an SM (C3-shape fit: 4 chunks at
+// ~100 registers 4.76 s, 2 chunks 4.27 s, 1 chunk at 6 blocks 5.84 s).
 // Per column the FMA chain runs over the entries in order, exactly as
 // k_gather, so results are bitwise equal.
-constexpr int kGvChunks = 4;
+constexpr int kGvChunks = 2;
 // nb > 1: a batch of independent gathers through the same projector, operand
 // b at src + b*sbs, in + b*ibs, out + b*obs (one launch for every target of a fit).
-__global__ void __launch_bounds__(kGatherWarps * 32)
+__global__ void __launch_bounds__(kGatherWarps * 32, 4)
     k_gather_f64v(int R, int c, int npass, const int* __restrict__ ptr, int k,
                   const int* __restrict__ idx, const double* __restrict__ val,
                   const double* __restrict__ src_base, long long lds, const double* in_base, long long ldi,
