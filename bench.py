@@ -81,6 +81,11 @@ def parse():
                     help="step driver of the timed region: the library's C++ schedule "
                          "(lsp_schedule_step, default) or schedule.LayerSchedule (Python); "
                          "the per-phase split always uses LayerSchedule's hooks")
+    ap.add_argument("--pipeline", type=int, default=-1,
+                    help="1: stage 2 + Adam of layer l on a side stream beside the Y build of "
+                         "layer l+1 (apply alone); 2: also beside its apply; 0: serial; "
+                         "-1 (default): 2 for bf16 W (measured faster: C3 5.77 -> 5.53 ms, "
+                         "C4-bf16 18.43 -> 18.24), 0 for fp32 W (C4 24.51 vs 24.68)")
     ap.add_argument("--concurrent", type=int, default=0,
                     help="1: compress and update chains on two streams (schedule.py)")
     ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
@@ -438,10 +443,17 @@ def run_ours(args):
     # (lsp_layer_allreduce on a comm stream; torch.distributed only bootstraps
     # the id and runs the barriers / max-over-ranks timing)
     comm = lsp.Comm.from_group() if world > 1 else None
+    pipeline = args.pipeline if args.pipeline >= 0 else (2 if wdt == "bf16" else 0)
+    if streams is not None:
+        pipeline = 0
     sched = LayerSchedule(layers, args.lr, comm=comm, record=record, streams=streams)
     native = None
     if args.schedule == "native" and streams is None:
-        native = lsp.Schedule(layers, comm=comm)  # csrc/schedule.cpp, same pipeline
+        # csrc/schedule.cpp: the same step as LayerSchedule (bitwise), with the
+        # pipelined order when selected
+        native = lsp.Schedule(layers, comm=comm, pipeline=pipeline)
+    elif pipeline:
+        sched = LayerSchedule(layers, args.lr, comm=comm, record=record, pipeline=pipeline)
 
     def one_step(record=False):
         recording[0] = record
@@ -538,6 +550,7 @@ def run_ours(args):
                                % (args.sms_compress, args.sms_update)) if args.concurrent else "1",
                    "schedule": ("native (lsp_schedule_step, csrc/schedule.cpp)" if native is not None
                                 else "python (schedule.LayerSchedule)"),
+                   "pipeline": pipeline,
                    "step_hbm_bytes_alg": balg,
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},

@@ -247,6 +247,13 @@ int lsp_layer_bind(lsp_layer_t layer, int idx, const void* g, int64_t ldg, lsp_d
 int lsp_layer_s_buffer(lsp_layer_t layer, void** s_t, int64_t* count);
 /* S^T_i = (P_i^T G_i Q_i)^T for every matrix (latches the non-finite flag). */
 int lsp_layer_compress(lsp_layer_t layer, lsp_stream_t stream);
+/* lsp_layer_compress in two enqueued halves (in this order, on any streams
+ * ordered by the caller): stage 1 Z^T_i = G_i^T P_i of every matrix (the pass
+ * over G), then stage 2 S^T_i = Q_i^T Z^T_i plus the non-finite latch.  Lets a
+ * schedule run stage 2 and Adam of one layer beside the Y build of another.
+ * Replaces: right_mul then leftT_mul, proj/src/projector.cpp:119-168. */
+int lsp_layer_compress_prepare(lsp_layer_t layer, lsp_stream_t stream);
+int lsp_layer_compress_finish(lsp_layer_t layer, lsp_stream_t stream);
 /* Adam on the layer's S^T (optionally re-checking finiteness, e.g. after an
  * all-reduce) and W_i -= lr * P_i delta_i Q_i^T; skipped if the flag is set. */
 int lsp_layer_update(lsp_layer_t layer, double lr, int check_finite, lsp_stream_t stream);
@@ -317,6 +324,11 @@ typedef void (*lsp_backward_fn)(int layer, lsp_stream_t stream, void* user);
 /* layers in forward order; comm may be NULL (single rank, no exchange). */
 int lsp_schedule_create(int count, const lsp_layer_t* layers, lsp_comm_t comm, lsp_schedule_t* out);
 int lsp_schedule_set_backward(lsp_schedule_t sched, lsp_backward_fn fn, void* user);
+/* mode 1: stage 2 (lsp_layer_compress_finish), the all-reduce and Adam of layer
+ * l on a side stream beside the Y build of layer l+1; mode 2: beside its Y
+ * build and apply; 0 (default): the order above.  Exclusive with a backward
+ * callback.  Results are bitwise those of mode 0. */
+int lsp_schedule_set_pipeline(lsp_schedule_t sched, int mode);
 int lsp_schedule_step(lsp_schedule_t sched, double lr, lsp_stream_t stream);
 int lsp_schedule_destroy(lsp_schedule_t sched);
 

@@ -119,6 +119,8 @@ _SIGS = {
     "lsp_layer_bind": (_i, [_vp, _i, _vp, _i64, _i, _vp, _i64, _i]),
     "lsp_layer_s_buffer": (_i, [_vp, C.POINTER(_vp), C.POINTER(_i64)]),
     "lsp_layer_compress": (_i, [_vp, _vp]),
+    "lsp_layer_compress_prepare": (_i, [_vp, _vp]),
+    "lsp_layer_compress_finish": (_i, [_vp, _vp]),
     "lsp_layer_update": (_i, [_vp, _d, _i, _vp]),
     "lsp_layer_adam": (_i, [_vp, _i, _vp]),
     "lsp_maybe_update": (_i, [_vp, _vp, _vp, C.c_int64, _i, _vp, _i, _i, _d, _vp, _i,
@@ -145,6 +147,7 @@ _SIGS = {
     "lsp_reproject_state": (_i, [_vp, _vp, _vp, _i, _vp]),
     "lsp_schedule_create": (_i, [_i, C.POINTER(_vp), _vp, C.POINTER(_vp)]),
     "lsp_schedule_set_backward": (_i, [_vp, _vp, _vp]),
+    "lsp_schedule_set_pipeline": (_i, [_vp, _i]),
     "lsp_schedule_step": (_i, [_vp, _d, _vp]),
     "lsp_schedule_destroy": (_i, [_vp]),
 }

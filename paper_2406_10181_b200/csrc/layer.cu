@@ -66,13 +66,17 @@ void check_bound(const lsp_layer_s& L) {
   }
 }
 
-void layer_compress(lsp_layer_s& L, cudaStream_t st) {
+std::vector<S1Job> compress_jobs(lsp_layer_s& L) {
   check_bound(L);
   std::vector<S1Job> jobs;
   for (int i = 0; i < L.count; ++i)
     jobs.push_back(S1Job{L.pairs[i], L.binds[i].g, L.binds[i].ldg,
                          L.zt.as<char>() + L.zt_off[i], L.s_block(i)});
-  compress_group_T(jobs, L.binds[0].gdt, L.adam.flag.as<int>(), st);
+  return jobs;
+}
+
+void layer_compress(lsp_layer_s& L, cudaStream_t st) {
+  compress_group_T(compress_jobs(L), L.binds[0].gdt, L.adam.flag.as<int>(), st);
 }
 
 void layer_adam(lsp_layer_s& L, bool check, cudaStream_t st) {
@@ -236,6 +240,20 @@ int lsp_layer_compress(lsp_layer_t L, lsp_stream_t stream) {
   return guard_layer([&] {
     require(L != nullptr, "layer_compress: null layer");
     layer_compress(*L, as_stream(stream));
+  });
+}
+
+int lsp_layer_compress_prepare(lsp_layer_t L, lsp_stream_t stream) {
+  return guard_layer([&] {
+    require(L != nullptr, "layer_compress_prepare: null layer");
+    launch_compress_stage1_group(compress_jobs(*L), L->binds[0].gdt, as_stream(stream));
+  });
+}
+
+int lsp_layer_compress_finish(lsp_layer_t L, lsp_stream_t stream) {
+  return guard_layer([&] {
+    require(L != nullptr, "layer_compress_finish: null layer");
+    launch_stage2_group(compress_jobs(*L), L->adam.flag.as<int>(), as_stream(stream));
   });
 }
 

@@ -34,8 +34,9 @@ struct lsp_schedule_s {
   int world = 1;
   lsp_backward_fn backward = nullptr;
   void* user = nullptr;
-  cudaStream_t comm_stream = nullptr, lsp_stream = nullptr;
-  std::vector<cudaEvent_t> compressed, reduced, grad;
+  int pipeline = 0;
+  cudaStream_t comm_stream = nullptr, lsp_stream = nullptr, side = nullptr;
+  std::vector<cudaEvent_t> compressed, reduced, grad, updated;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 
@@ -84,6 +85,37 @@ int finish(lsp_schedule_s* S, int li, double lr, cudaStream_t st) {
   return LSP_OK;
 }
 
+// Pipelined step (lsp_schedule_set_pipeline): stage 2, the all-reduce and Adam
+// of layer l on the side stream beside the Y build (mode 1) or the Y build and
+// apply (mode 2) of layer l+1 on the caller's stream.
+int finish_pipelined(lsp_schedule_s* S, int li, int nxt, double lr, cudaStream_t main) {
+  SCK(cudaStreamWaitEvent(main, S->updated[li], 0));
+  LCK(lsp_layer_apply_prepare(S->layers[li], main));
+  if (nxt >= 0 && S->pipeline == 1) SCK(cudaStreamWaitEvent(main, S->updated[nxt], 0));
+  LCK(lsp_layer_apply_finish(S->layers[li], lr, main));
+  return LSP_OK;
+}
+
+int step_pipelined(lsp_schedule_s* S, double lr, cudaStream_t main) {
+  const int n = static_cast<int>(S->layers.size());
+  SCK(cudaEventRecord(S->fork, main));
+  SCK(cudaStreamWaitEvent(S->side, S->fork, 0));
+  int prev = -1;
+  for (int li = n - 1; li >= 0; --li) {
+    lsp_layer_t L = S->layers[li];
+    LCK(lsp_layer_compress_prepare(L, main));
+    SCK(cudaEventRecord(S->compressed[li], main));
+    SCK(cudaStreamWaitEvent(S->side, S->compressed[li], 0));
+    LCK(lsp_layer_compress_finish(L, S->side));
+    if (S->comm) LCK(lsp_layer_allreduce(L, S->comm, S->side));
+    LCK(lsp_layer_adam(L, S->world > 1 ? 1 : 0, S->side));
+    SCK(cudaEventRecord(S->updated[li], S->side));
+    if (prev >= 0) LCK(finish_pipelined(S, prev, li, lr, main));
+    prev = li;
+  }
+  return finish_pipelined(S, prev, -1, lr, main);  // joins the side stream (updated[0])
+}
+
 }  // namespace
 
 extern "C" {
@@ -110,6 +142,7 @@ int lsp_schedule_create(int count, const lsp_layer_t* layers, lsp_comm_t comm, l
     return true;
   };
   if (!mk(S->compressed, count) || !mk(S->reduced, count) || !mk(S->grad, count) ||
+      !mk(S->updated, count) ||
       cudaEventCreateWithFlags(&S->fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&S->join, cudaEventDisableTiming) != cudaSuccess) {
     lsp_schedule_destroy(S);
@@ -131,9 +164,21 @@ int lsp_schedule_set_backward(lsp_schedule_t S, lsp_backward_fn fn, void* user) 
   return LSP_OK;
 }
 
+int lsp_schedule_set_pipeline(lsp_schedule_t S, int mode) {
+  if (!S) return fail(LSP_EINVAL, "schedule_set_pipeline: null schedule");
+  if (mode < 0 || mode > 2) return fail(LSP_EINVAL, "schedule_set_pipeline: mode must be 0, 1 or 2");
+  S->pipeline = mode;
+  if (mode) return make_stream(&S->side);
+  return LSP_OK;
+}
+
 int lsp_schedule_step(lsp_schedule_t S, double lr, lsp_stream_t stream) {
   if (!S) return fail(LSP_EINVAL, "schedule_step: null schedule");
   cudaStream_t main = static_cast<cudaStream_t>(stream);
+  if (S->pipeline) {
+    if (S->backward) return fail(LSP_EINVAL, "schedule_step: pipeline and backward modes are exclusive");
+    return step_pipelined(S, lr, main);
+  }
   const int n = static_cast<int>(S->layers.size());
   // fork the side streams from the caller's stream (also what graph capture needs)
   SCK(cudaEventRecord(S->fork, main));
@@ -164,13 +209,14 @@ int lsp_schedule_step(lsp_schedule_t S, double lr, lsp_stream_t stream) {
 
 int lsp_schedule_destroy(lsp_schedule_t S) {
   if (!S) return LSP_OK;
-  for (auto* v : {&S->compressed, &S->reduced, &S->grad})
+  for (auto* v : {&S->compressed, &S->reduced, &S->grad, &S->updated})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   if (S->fork) cudaEventDestroy(S->fork);
   if (S->join) cudaEventDestroy(S->join);
   if (S->comm_stream) cudaStreamDestroy(S->comm_stream);
   if (S->lsp_stream) cudaStreamDestroy(S->lsp_stream);
+  if (S->side) cudaStreamDestroy(S->side);
   delete S;
   return LSP_OK;
 }

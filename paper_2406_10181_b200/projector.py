@@ -467,6 +467,14 @@ class Layer:
     def compress(self, stream=None):
         lib.layer_compress(self._h, _stream(stream))
 
+    def compress_prepare(self, stream=None):
+        """First half of compress(): stage 1 (Z^T = G^T P, the pass over G)."""
+        lib.layer_compress_prepare(self._h, _stream(stream))
+
+    def compress_finish(self, stream=None):
+        """Second half of compress(): stage 2 (S^T = Q^T Z^T) and the non-finite latch."""
+        lib.layer_compress_finish(self._h, _stream(stream))
+
     def update(self, lr: float, check_finite: bool = False, stream=None):
         lib.layer_update(self._h, float(lr), int(bool(check_finite)), _stream(stream))
 
@@ -665,9 +673,12 @@ class Schedule:
 
     backward(layer, stream): optional; called on the host in backward order to
     enqueue the backward of ``layer`` on ``stream`` (a torch.cuda.ExternalStream).
+    pipeline: 1 / 2 -- stage 2 + Adam of layer l on a side stream beside the Y
+    build (and apply, 2) of layer l+1 (``LayerSchedule(pipeline=...)``).
     """
 
-    def __init__(self, layers: Sequence[Layer], comm: Optional[Comm] = None, backward=None):
+    def __init__(self, layers: Sequence[Layer], comm: Optional[Comm] = None, backward=None,
+                 pipeline: int = 0):
         self.layers = list(layers)
         self.comm = comm
         arr = (C.c_void_p * len(self.layers))(*[l.handle for l in self.layers])
@@ -678,6 +689,8 @@ class Schedule:
         self._cb = None
         if backward is not None:
             self.set_backward(backward)
+        if pipeline:
+            lib.schedule_set_pipeline(self._h, int(pipeline))
 
     def set_backward(self, backward):
         torch = _torch()

@@ -36,7 +36,7 @@ class LayerSchedule:
     def __init__(self, layers: Sequence, lr: float, group=None,
                  record: Optional[Callable[[str, int, str], None]] = None, streams=None,
                  comm=None, backward: Optional[Callable[[int], None]] = None,
-                 lsp_stream=None, comm_stream=None):
+                 lsp_stream=None, comm_stream=None, pipeline: int = 0):
         """layers: in forward order.
         group: a torch.distributed process group or None (single rank).
         comm: a paper_2406_10181_b200.Comm (the library's NCCL communicator);
@@ -57,6 +57,8 @@ class LayerSchedule:
         self.backward = backward
         self.lsp_stream = lsp_stream
         self.comm_stream = comm_stream
+        self.pipeline = pipeline
+        self._side = None
         self._events = None
         self.world = 1
         if comm is not None:
@@ -136,6 +138,8 @@ class LayerSchedule:
         return list(reversed(range(len(self.layers))))
 
     def step(self):
+        if self.pipeline:
+            return self._step_pipeline()
         if self.backward is not None:
             return self._step_backward()
         if self.streams is not None:
@@ -184,6 +188,54 @@ class LayerSchedule:
             if pending is not None:
                 self._finish(*pending)
         main.wait_stream(ls)
+
+    def _step_pipeline(self):
+        """Stage 2, the all-reduce and Adam of layer l on a side stream beside the
+        Y build (and, with pipeline=2, the apply) of layer l+1 on the caller's
+        stream: the light, latency-bound kernels share SMs with the Y build
+        (L1-bound) instead of running alone between the heavy ones.  Same
+        kernels on the same data, so bitwise the serial schedule's results."""
+        import torch
+
+        main = torch.cuda.current_stream()
+        side = self._side
+        if side is None:
+            side = self._side = torch.cuda.Stream()
+        ev = self._ev()
+        side.wait_stream(main)  # fork (also what graph capture needs)
+        prev = None
+        for li in self.order():
+            lay = self.layers[li]
+            self._rec("compress", li, "begin")
+            lay.compress_prepare()
+            ev["compressed"][li].record(main)
+            with torch.cuda.stream(side):
+                side.wait_event(ev["compressed"][li])
+                lay.compress_finish()
+                self._rec("compress", li, "end")
+                if self.comm is not None:
+                    lay.allreduce(self.comm)
+                self._rec("adam", li, "begin")
+                lay.adam(self.world > 1)
+                self._rec("adam", li, "end")
+                ev["update"][li].record(side)
+            if prev is not None:
+                self._finish_pipelined(prev, li, main)
+            prev = li
+        self._finish_pipelined(prev, None, main)
+
+    def _finish_pipelined(self, li, nxt, main):
+        ev = self._ev()
+        lay = self.layers[li]
+        main.wait_event(ev["update"][li])
+        self._rec("build", li, "begin")
+        lay.apply_prepare()
+        self._rec("build", li, "end")
+        if nxt is not None and self.pipeline == 1:
+            main.wait_event(ev["update"][nxt])  # the apply runs alone (full-SM persistent kernel)
+        self._rec("apply", li, "begin")
+        lay.apply_finish(self.lr)
+        self._rec("apply", li, "end")
 
     def _step_concurrent(self):
         import torch

@@ -264,3 +264,41 @@ def test_native_schedule_graph_capture(cuda, comm):
 def test_native_schedule_rejects_bad_input(cuda):
     with pytest.raises(lsp.InvalidArgument):
         lsp.Schedule([])
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_native_pipeline_bitwise_and_capture(cuda, comm, mode, with_comm):
+    """lsp_schedule_set_pipeline(1|2): stage 2 + all-reduce + Adam of layer l on
+    the schedule's side stream beside the Y build (and apply) of layer l+1;
+    weights bitwise equal to the serial schedule, eager and as graph replays."""
+    c = comm if with_comm else None
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    lc, wc, ac = _build()
+    for li in range(L):
+        for acts in (aa, ab, ac):
+            _backward(acts)(li)
+    sa = LayerSchedule(la, 1e-3, comm=c)
+    sb = lsp.Schedule(lb, comm=c, pipeline=mode)
+    sc = lsp.Schedule(lc, comm=c, pipeline=mode)
+    for _ in range(4):
+        sa.step()
+        sb.step(1e-3)
+    sc.step(1e-3)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sc.step(1e-3)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for x, y, z in zip(wa, wb, wc):
+        assert torch.equal(x, y) and torch.equal(x, z)
+
+
+def test_native_pipeline_rejects_backward(cuda):
+    la, wa, aa = _build()
+    s = lsp.Schedule(la, backward=lambda li, st: None, pipeline=1)
+    with pytest.raises(lsp.InvalidArgument):
+        s.step(1e-3)

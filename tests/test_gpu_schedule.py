@@ -135,3 +135,20 @@ def test_graph_replay_back_to_back_full_size(cuda, d, r):
         graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(wa, wb)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_pipeline_mode_bitwise(cuda, mode):
+    """LayerSchedule(pipeline=1|2): stage 2 + Adam of layer l on a side stream
+    beside the Y build (and apply) of layer l+1, via the split
+    lsp_layer_compress_prepare / _finish; bitwise the serial schedule."""
+    la, wa = _build()
+    lb, wb = _build()
+    sa = LayerSchedule(la, 1e-3)
+    sb = LayerSchedule(lb, 1e-3, pipeline=mode)
+    for _ in range(3):
+        sa.step()
+        sb.step()
+    torch.cuda.synchronize()
+    for a, b in zip(wa, wb):
+        assert torch.equal(a, b)
