@@ -124,3 +124,8 @@ def test_schedule_rejects_bad_args():
     with pytest.raises(lsp.InvalidArgument):
         lsp.lib.schedule_step(None, 1e-3, None)
     lsp.lib.schedule_destroy(None)  # a null handle is a no-op
+
+
+def test_schedule_set_pipeline_rejects_bad_args():
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.schedule_set_pipeline(None, 1)
