@@ -26,6 +26,14 @@ or gloo sum-then-scale for the CPU stand-in tests).
 Anything that exposes ``compress()``, ``s_buffer()``, ``adam(check)`` and
 ``apply(lr)`` can be scheduled: ``paper_2406_10181_b200.Layer`` on the GPU, or a
 CPU stand-in (tests/test_dist_cpu.py runs this exact class over gloo).
+
+``pipeline=1|2`` moves stage 2 (``compress_finish``), the all-reduce and Adam of
+layer l onto a side stream beside the Y build (and, 2, the apply) of layer l+1
+(faster for bf16 W).  The library's native twin of this class is
+``paper_2406_10181_b200.Schedule`` (csrc/schedule.cpp, lsp_schedule_*), which
+bench.py times; the two enqueue the same kernels in the same order (bitwise
+equal results, tests/test_gpu_comm_overlap.py), this one adds the per-stage
+``record`` hooks used for the phase split.
 """
 from __future__ import annotations
 
