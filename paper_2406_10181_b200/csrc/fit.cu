@@ -156,34 +156,59 @@ __global__ void k_poly_tile(int d, long long dd, const double* s0, const double*
   }
 }
 
-// <A1, A2> with A2 given as A2^T (row-major), one 32 x 32 tile per block
-// (A2^T tile staged transposed through shared memory), gridDim.z = target;
-// per-block partials in fixed order.  Replaces the A2 transpose + dot pass.
-__global__ void k_dot_tile(int d, long long dd, const double* __restrict__ a1,
-                           const double* __restrict__ a2t, double* __restrict__ partials) {
-  __shared__ double tile[32][33];
-  __shared__ double red[256];
-  const long long off = static_cast<long long>(blockIdx.z) * dd;
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // A1 tile: rows by.., cols bx..
-  for (int y = threadIdx.y; y < 32; y += 8) {
-    const int r = bx + y, c = by + threadIdx.x;  // A2^T[r][c] = A2[c][r]
-    tile[y][threadIdx.x] = (r < d && c < d) ? a2t[off + static_cast<long long>(r) * d + c] : 0.0;
-  }
-  __syncthreads();
+// <Gp S, S Gq> = <Q A1^T, Q S^T> (A1 = Gp S): per row j of Q, u = sum_l q_jl
+// A1^T[pos_jl] and w = sum_l q_jl S^T[pos_jl] (row gathers of the L2-resident
+// d x d operands, never written) and u . w; one warp per row, gridDim.y =
+// target, per-block partials in fixed order (partials[y][block]).  Replaces the
+// n x d intermediate Q S^T, its CSC gather and a dot-product pass.
+constexpr int kQdWarps = 8;
+__global__ void __launch_bounds__(kQdWarps * 32)
+    k_qdot(int d, int n, int k, long long dd, const int* __restrict__ pos, const double* __restrict__ val,
+           const double* __restrict__ a1t, const double* __restrict__ st, double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long off = static_cast<long long>(blockIdx.y) * dd;
   double acc = 0.0;
-  for (int y = threadIdx.y; y < 32; y += 8) {
-    const int r = by + y, c = bx + threadIdx.x;  // A1[r][c] * A2[r][c], A2[r][c] = tile[c-bx][r-by]
-    if (r < d && c < d) acc = fma(a1[off + static_cast<long long>(r) * d + c], tile[threadIdx.x][y], acc);
+  for (int j = blockIdx.x * kQdWarps + warp; j < n; j += gridDim.x * kQdWarps) {
+    const int* pj = pos + static_cast<long long>(j) * k;
+    const double* vj = val + static_cast<long long>(j) * k;
+    if ((d & 1) == 0) {
+      for (int c = 2 * lane; c < d; c += 64) {
+        double2 u = make_double2(0.0, 0.0), w = make_double2(0.0, 0.0);
+        for (int l = 0; l < k; ++l) {
+          const long long row = off + static_cast<long long>(__ldg(pj + l)) * d + c;
+          const double q = __ldg(vj + l);
+          const double2 x = __ldg(reinterpret_cast<const double2*>(a1t + row));
+          const double2 y = __ldg(reinterpret_cast<const double2*>(st + row));
+          u.x = fma(q, x.x, u.x), u.y = fma(q, x.y, u.y);
+          w.x = fma(q, y.x, w.x), w.y = fma(q, y.y, w.y);
+        }
+        acc = fma(u.x, w.x, fma(u.y, w.y, acc));
+      }
+    } else {
+      for (int c = lane; c < d; c += 32) {
+        double u = 0.0, w = 0.0;
+        for (int l = 0; l < k; ++l) {
+          const long long row = off + static_cast<long long>(__ldg(pj + l)) * d + c;
+          const double q = __ldg(vj + l);
+          u = fma(q, a1t[row], u);
+          w = fma(q, st[row], w);
+        }
+        acc = fma(u, w, acc);
+      }
+    }
   }
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  red[tid] = acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[kQdWarps];
+  if (lane == 0) red[warp] = acc;
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     double x = 0.0;
-    for (int i = 0; i < 256; ++i) x += red[i];
-    partials[static_cast<long long>(blockIdx.z) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = x;
+    for (int i = 0; i < kQdWarps; ++i) x += red[i];
+    partials[static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x] = x;
   }
 }
+constexpr int kQdBlocks = 296;  // per target
 
 // out (da x db, row-major) = A^T B for two projectors over the same rows, in
 // the reference's summation order (rows ascending per output entry,
@@ -372,7 +397,7 @@ struct FitEngine {
   std::unique_ptr<lsp_projector_s> P, Q, Pd, Qd;  // Pd, Qd: the descent direction's values
   // per target (contiguous, target-major): S^T(t) = s0T - t s1T + t^2 s2T, and the
   // batched loss intermediates
-  DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, bqs, ba2T;
+  DevBuf s0T, s1T, s2T, bsT, bs, bu, ba1, ba2T;
   DevBuf zt_all;  // per target Z^T = G^T P of the last gradient (reused by prepare_line)
   DevBuf dgp, dgq;  // gradient accumulators (values layout)
   std::vector<DevBuf> g, gT;  // fp64 targets and transposes
@@ -481,13 +506,12 @@ struct FitEngine {
   }
 
   void bias2_from_bsT(double line_t) {
-    const size_t dd = static_cast<size_t>(d) * d, md = static_cast<size_t>(m) * d,
-                 nd = static_cast<size_t>(n) * d;
+    const size_t dd = static_cast<size_t>(d) * d, md = static_cast<size_t>(m) * d;
     bs.ensure(T * dd * 8), ba1.ensure(T * dd * 8), ba2T.ensure(T * dd * 8);
-    bu.ensure(T * md * 8), bqs.ensure(T * nd * 8);
+    bu.ensure(T * md * 8);
     const int tiles = ceil_div(d, 32);
     const size_t np = static_cast<size_t>(tiles) * tiles;
-    lparts.ensure(T * 2 * np * sizeof(double));
+    lparts.ensure(T * (np + kQdBlocks) * sizeof(double));
     double* ss_parts = lparts.as<double>();
     double* ag_parts = lparts.as<double>() + T * np;
     const dim3 tg(tiles, tiles, T), tb(32, 8);
@@ -497,13 +521,14 @@ struct FitEngine {
                                    line_t >= 0.0 ? s2T.as<double>() : nullptr, line_t, bsT.as<double>(),
                                    bs.as<double>(), ss_parts);
     after_launch("poly_tile");
-    const double* sTp = bsT.as<double>();
     gather_batch(*P, true, bs.as<double>(), dd, bu.as<double>(), md);      // U    = P S
     gather_batch(*P, false, bu.as<double>(), md, ba1.as<double>(), dd);    // A1   = Gp S
-    gather_batch(*Q, true, sTp, dd, bqs.as<double>(), nd);                 // Q S^T
-    gather_batch(*Q, false, bqs.as<double>(), nd, ba2T.as<double>(), dd);  // A2^T = Gq S^T
-    k_dot_tile<<<tg, tb, 0, st>>>(d, static_cast<long long>(dd), ba1.as<double>(), ba2T.as<double>(), ag_parts);
-    after_launch("dot_tile");
+    double* a1t = ba2T.as<double>();                                      // (buffer reuse)
+    launch_transpose_batch(d, d, ba1.as<double>(), d, dd, a1t, d, dd, T, st);  // A1^T
+    k_qdot<<<dim3(kQdBlocks, T), kQdWarps * 32, 0, st>>>(d, n, Q->r, static_cast<long long>(dd),
+                                                          Q->pos.as<int>(), Q->val.as<double>(), a1t,
+                                                          bsT.as<double>(), ag_parts);
+    after_launch("qdot");
   }
 
   // all targets' |b_i|^2 with one synchronisation (clamped at 0: the identity
@@ -517,16 +542,14 @@ struct FitEngine {
     bias2_from_bsT(line_t);
     const int tiles = ceil_div(d, 32);
     const size_t np = static_cast<size_t>(tiles) * tiles;
-    std::vector<double> h(T * 2 * np);
+    std::vector<double> h(T * (np + kQdBlocks));
     LSP_CUDA(cudaMemcpyAsync(h.data(), lparts.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     LSP_CUDA(cudaStreamSynchronize(st));
     std::vector<double> out(T);
     for (int i = 0; i < T; ++i) {
       double ss = 0.0, ag = 0.0;
-      for (size_t b = 0; b < np; ++b) {
-        ss += h[i * np + b];
-        ag += h[T * np + i * np + b];
-      }
+      for (size_t b = 0; b < np; ++b) ss += h[i * np + b];
+      for (int b = 0; b < kQdBlocks; ++b) ag += h[T * np + static_cast<size_t>(i) * kQdBlocks + b];
       out[i] = std::max(0.0, gnorm2[i] - 2.0 * ss + ag);
     }
     return out;
