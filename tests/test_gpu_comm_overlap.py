@@ -302,3 +302,38 @@ def test_native_pipeline_rejects_backward(cuda):
     s = lsp.Schedule(la, backward=lambda li, st: None, pipeline=1)
     with pytest.raises(lsp.InvalidArgument):
         s.step(1e-3)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_native_schedule_nonfinite_layer_skipped(cuda, comm, mode):
+    """A non-finite gradient in one layer (reference: NumericError before any
+    state change, subspace_opt.cpp:38): with the native schedule in every order
+    (stage 2 latching the flag on the side stream in the pipelined ones), that
+    layer's W is untouched, the other layers are updated exactly as without the
+    bad layer, and lsp_layer_check raises NumericError."""
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    for li in range(L):
+        _backward(aa)(li)
+        _backward(ab)(li)
+    bad = 1
+    ab[bad][0][2][0, 0] = float("nan")  # G of the bad layer's first matrix
+    w0 = [w.clone() for w in wb]
+    sa = LayerSchedule(la, 1e-3)
+    sb = lsp.Schedule(lb, comm=comm, pipeline=mode)
+    sa.step()
+    sb.step(1e-3)
+    torch.cuda.synchronize()
+    per = len(SHAPES)
+    for li in range(L):
+        for i in range(per):
+            k = li * per + i
+            if li == bad:
+                assert torch.equal(wb[k], w0[k])
+            else:
+                assert torch.equal(wa[k], wb[k])
+    with pytest.raises(lsp.NumericError):
+        lb[bad].check()
+    for li in range(L):
+        if li != bad:
+            lb[li].check()
