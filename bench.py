@@ -88,6 +88,10 @@ def parse():
                          "C4-bf16 18.43 -> 18.24), 0 for fp32 W (C4 24.51 vs 24.68)")
     ap.add_argument("--concurrent", type=int, default=0,
                     help="1: compress and update chains on two streams (schedule.py)")
+    ap.add_argument("--partition", type=int, default=0,
+                    help="SMs of the green-context partition running every layer's compress "
+                         "stage 1 while the rest run stage 2 / Adam / Y build / apply "
+                         "(lsp_schedule_set_partition; native schedule only); 0: off")
     ap.add_argument("--sms-compress", type=int, default=0, help="lsp_set_sm_budget compress SMs")
     ap.add_argument("--sms-update", type=int, default=0, help="lsp_set_sm_budget update SMs")
     ap.add_argument("--overlap-bwd", type=int, default=0, metavar="TOKENS",
@@ -451,7 +455,8 @@ def run_ours(args):
     if args.schedule == "native" and streams is None:
         # csrc/schedule.cpp: the same step as LayerSchedule (bitwise), with the
         # pipelined order when selected
-        native = lsp.Schedule(layers, comm=comm, pipeline=pipeline)
+        native = lsp.Schedule(layers, comm=comm, pipeline=0 if args.partition else pipeline,
+                              partition=args.partition)
     elif pipeline:
         sched = LayerSchedule(layers, args.lr, comm=comm, record=record, pipeline=pipeline)
 
@@ -551,6 +556,8 @@ def run_ours(args):
                    "schedule": ("native (lsp_schedule_step, csrc/schedule.cpp)" if native is not None
                                 else "python (schedule.LayerSchedule)"),
                    "pipeline": pipeline,
+                   "partition_sms": (list(native.partition) if native is not None and args.partition
+                                     else None),
                    "step_hbm_bytes_alg": balg,
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},

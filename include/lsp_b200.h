@@ -329,6 +329,16 @@ int lsp_schedule_set_backward(lsp_schedule_t sched, lsp_backward_fn fn, void* us
  * build and apply; 0 (default): the order above.  Exclusive with a backward
  * callback.  Results are bitwise those of mode 0. */
 int lsp_schedule_set_pipeline(lsp_schedule_t sched, int mode);
+/* Spatial partition: split the device's SMs into two green contexts,
+ * `compress_sms` (rounded up by the driver: multiples of 8 on sm_100) running
+ * stage 1 of every layer back to back, the rest running, per layer as soon as
+ * its stage 1 is done, stage 2, the all-reduce, Adam, the Y build and the
+ * apply (the L2-bound compress and the HBM-bound apply side by side on
+ * disjoint SMs).  0 removes the partition.  got_compress / got_update (may be
+ * NULL) receive the SM counts provisioned.  Exclusive with the backward and
+ * pipeline modes; same kernels on the same data, so bitwise the results of
+ * mode 0. */
+int lsp_schedule_set_partition(lsp_schedule_t sched, int compress_sms, int* got_compress, int* got_update);
 int lsp_schedule_step(lsp_schedule_t sched, double lr, lsp_stream_t stream);
 int lsp_schedule_destroy(lsp_schedule_t sched);
 

@@ -148,6 +148,7 @@ _SIGS = {
     "lsp_schedule_create": (_i, [_i, C.POINTER(_vp), _vp, C.POINTER(_vp)]),
     "lsp_schedule_set_backward": (_i, [_vp, _vp, _vp]),
     "lsp_schedule_set_pipeline": (_i, [_vp, _i]),
+    "lsp_schedule_set_partition": (_i, [_vp, _i, C.POINTER(_i), C.POINTER(_i)]),
     "lsp_schedule_step": (_i, [_vp, _d, _vp]),
     "lsp_schedule_destroy": (_i, [_vp]),
 }

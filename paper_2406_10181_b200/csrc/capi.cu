@@ -48,6 +48,14 @@ int num_sms() {
 
 std::atomic<int> g_budget[2] = {{0}, {0}};
 
+// lsp_schedule_set_partition: persistent grids sized for the partition while a
+// partitioned step is enqueued (host side, one thread)
+void budget_exchange(int compress_sms, int update_sms, int* old_compress, int* old_update) {
+  const int c = g_budget[0].exchange(compress_sms), u = g_budget[1].exchange(update_sms);
+  if (old_compress) *old_compress = c;
+  if (old_update) *old_update = u;
+}
+
 int sm_budget(int phase) {
   const int b = g_budget[phase].load(std::memory_order_relaxed);
   return b > 0 ? std::min(b, num_sms()) : num_sms();

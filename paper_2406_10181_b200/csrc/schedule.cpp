@@ -17,6 +17,8 @@
 // joined back into the caller's stream by events, so a step can be captured in
 // a CUDA graph.  Same order of operations as paper_2406_10181_b200/schedule.py
 // (LayerSchedule), hence bitwise the same results.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -26,6 +28,7 @@
 
 namespace lspb {
 extern thread_local std::string g_last_error;
+void budget_exchange(int compress_sms, int update_sms, int* old_compress, int* old_update);
 }
 
 struct lsp_schedule_s {
@@ -38,6 +41,10 @@ struct lsp_schedule_s {
   cudaStream_t comm_stream = nullptr, lsp_stream = nullptr, side = nullptr;
   std::vector<cudaEvent_t> compressed, reduced, grad, updated;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // spatial partition (lsp_schedule_set_partition): two green contexts
+  int part_c = 0, part_u = 0;
+  CUgreenCtx green_c = nullptr, green_u = nullptr;
+  cudaStream_t pc = nullptr, pu = nullptr;
 };
 
 namespace {
@@ -116,6 +123,123 @@ int step_pipelined(lsp_schedule_s* S, double lr, cudaStream_t main) {
   return finish_pipelined(S, prev, -1, lr, main);  // joins the side stream (updated[0])
 }
 
+// Partitioned step (lsp_schedule_set_partition): stage 1 of every layer back
+// to back on the compress partition's stream, and on the update partition's
+// stream, per layer as soon as its stage 1 is done: stage 2, the all-reduce,
+// Adam, the Y build and the apply.  Stage 1 is bound by L2 gathers (G crosses
+// HBM once at ~2.8 TB/s) and the apply by HBM, and neither keeps its rate
+// linear in SMs (measured: compress on half the SMs 1.5x, apply 1.6x slower),
+// which made two disjoint SM sets running the chains side by side look
+// promising; measured, the co-running chains slow each other through the
+// shared L2 and HBM and the step is no faster than the serial order (C4 fp32
+// 24.57 vs 24.42 ms at 64 | 84 SMs; profiles/r02_notes.md), so the partition
+// is opt-in.  Persistent grids are sized for their partition while the step
+// is enqueued.
+int step_partitioned(lsp_schedule_s* S, double lr, cudaStream_t main) {
+  const int n = static_cast<int>(S->layers.size());
+  SCK(cudaEventRecord(S->fork, main));
+  SCK(cudaStreamWaitEvent(S->pc, S->fork, 0));
+  SCK(cudaStreamWaitEvent(S->pu, S->fork, 0));
+  int oc = 0, ou = 0;
+  lspb::budget_exchange(S->part_c, S->part_u, &oc, &ou);
+  int rc = LSP_OK;
+  for (int li = n - 1; li >= 0 && rc == LSP_OK; --li) {
+    rc = lsp_layer_compress_prepare(S->layers[li], S->pc);
+    if (rc == LSP_OK && cudaEventRecord(S->compressed[li], S->pc) != cudaSuccess)
+      rc = fail(LSP_ECUDA, "schedule: event record on the compress partition failed");
+  }
+  for (int li = n - 1; li >= 0 && rc == LSP_OK; --li) {
+    lsp_layer_t L = S->layers[li];
+    if (cudaStreamWaitEvent(S->pu, S->compressed[li], 0) != cudaSuccess) {
+      rc = fail(LSP_ECUDA, "schedule: wait on the compress partition failed");
+      break;
+    }
+    rc = lsp_layer_compress_finish(L, S->pu);
+    if (rc == LSP_OK && S->comm) rc = lsp_layer_allreduce(L, S->comm, S->pu);
+    if (rc == LSP_OK) rc = lsp_layer_adam(L, S->world > 1 ? 1 : 0, S->pu);
+    if (rc == LSP_OK) rc = lsp_layer_apply(L, lr, S->pu);
+  }
+  lspb::budget_exchange(oc, ou, nullptr, nullptr);
+  LCK(rc);
+  // the update stream waited on the last stage 1, so joining it joins both
+  SCK(cudaEventRecord(S->join, S->pu));
+  SCK(cudaStreamWaitEvent(main, S->join, 0));
+  return LSP_OK;
+}
+
+template <typename F>
+bool driver_fn(const char* name, F* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  *out = reinterpret_cast<F>(fn);
+  return true;
+}
+
+void drop_partition(lsp_schedule_s* S) {
+  PFN_cuGreenCtxDestroy destroy = nullptr;
+  driver_fn("cuGreenCtxDestroy", &destroy);
+  if (S->pc) cudaStreamDestroy(S->pc);
+  if (S->pu) cudaStreamDestroy(S->pu);
+  if (destroy) {
+    if (S->green_c) destroy(S->green_c);
+    if (S->green_u) destroy(S->green_u);
+  }
+  S->pc = S->pu = nullptr;
+  S->green_c = S->green_u = nullptr;
+  S->part_c = S->part_u = 0;
+}
+
+int make_partition(lsp_schedule_s* S, int compress_sms) {
+  PFN_cuDeviceGet dev_get = nullptr;
+  PFN_cuDeviceGetDevResource get_res = nullptr;
+  PFN_cuDevSmResourceSplitByCount split = nullptr;
+  PFN_cuDevResourceGenerateDesc gen = nullptr;
+  PFN_cuGreenCtxCreate create = nullptr;
+  PFN_cuGreenCtxStreamCreate stream_create = nullptr;
+  if (!driver_fn("cuDeviceGet", &dev_get) || !driver_fn("cuDeviceGetDevResource", &get_res) ||
+      !driver_fn("cuDevSmResourceSplitByCount", &split) || !driver_fn("cuDevResourceGenerateDesc", &gen) ||
+      !driver_fn("cuGreenCtxCreate", &create) || !driver_fn("cuGreenCtxStreamCreate", &stream_create))
+    return fail(LSP_ECUDA, "schedule_set_partition: the driver has no green-context API");
+  int ordinal = 0;
+  SCK(cudaGetDevice(&ordinal));
+  SCK(cudaFree(nullptr));  // the primary context exists before the green ones
+  CUdevice dev;
+  CUdevResource all{}, part{}, rest{};
+  CUdevResourceDesc dc = nullptr, du = nullptr;
+  unsigned groups = 1;
+  auto bad = [&](const char* what) { return fail(LSP_ECUDA, std::string("schedule_set_partition: ") + what); };
+  if (dev_get(&dev, ordinal) != CUDA_SUCCESS) return bad("cuDeviceGet");
+  if (get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return bad("cuDeviceGetDevResource");
+  if (compress_sms >= static_cast<int>(all.sm.smCount))
+    return fail(LSP_EINVAL, "schedule_set_partition: the compress partition must leave SMs for the update");
+  if (split(&part, &groups, &all, &rest, 0, static_cast<unsigned>(compress_sms)) != CUDA_SUCCESS || groups != 1 ||
+      rest.sm.smCount == 0)
+    return bad("cuDevSmResourceSplitByCount");
+  if (gen(&dc, &part, 1) != CUDA_SUCCESS || gen(&du, &rest, 1) != CUDA_SUCCESS) return bad("cuDevResourceGenerateDesc");
+  if (create(&S->green_c, dc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      create(&S->green_u, du, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    drop_partition(S);
+    return bad("cuGreenCtxCreate");
+  }
+  CUstream a = nullptr, b = nullptr;
+  if (stream_create(&a, S->green_c, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      stream_create(&b, S->green_u, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    if (a) cudaStreamDestroy(a);
+    drop_partition(S);
+    return bad("cuGreenCtxStreamCreate");
+  }
+  S->pc = a;
+  S->pu = b;
+  S->part_c = static_cast<int>(part.sm.smCount);
+  S->part_u = static_cast<int>(rest.sm.smCount);
+  return LSP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -172,9 +296,24 @@ int lsp_schedule_set_pipeline(lsp_schedule_t S, int mode) {
   return LSP_OK;
 }
 
+int lsp_schedule_set_partition(lsp_schedule_t S, int compress_sms, int* got_compress, int* got_update) {
+  if (!S) return fail(LSP_EINVAL, "schedule_set_partition: null schedule");
+  if (compress_sms < 0) return fail(LSP_EINVAL, "schedule_set_partition: negative SM count");
+  drop_partition(S);
+  if (compress_sms > 0) LCK(make_partition(S, compress_sms));
+  if (got_compress) *got_compress = S->part_c;
+  if (got_update) *got_update = S->part_u;
+  return LSP_OK;
+}
+
 int lsp_schedule_step(lsp_schedule_t S, double lr, lsp_stream_t stream) {
   if (!S) return fail(LSP_EINVAL, "schedule_step: null schedule");
   cudaStream_t main = static_cast<cudaStream_t>(stream);
+  if (S->part_c) {
+    if (S->backward || S->pipeline)
+      return fail(LSP_EINVAL, "schedule_step: the partitioned step excludes backward and pipeline modes");
+    return step_partitioned(S, lr, main);
+  }
   if (S->pipeline) {
     if (S->backward) return fail(LSP_EINVAL, "schedule_step: pipeline and backward modes are exclusive");
     return step_pipelined(S, lr, main);
@@ -217,6 +356,7 @@ int lsp_schedule_destroy(lsp_schedule_t S) {
   if (S->comm_stream) cudaStreamDestroy(S->comm_stream);
   if (S->lsp_stream) cudaStreamDestroy(S->lsp_stream);
   if (S->side) cudaStreamDestroy(S->side);
+  drop_partition(S);
   delete S;
   return LSP_OK;
 }

@@ -675,10 +675,13 @@ class Schedule:
     enqueue the backward of ``layer`` on ``stream`` (a torch.cuda.ExternalStream).
     pipeline: 1 / 2 -- stage 2 + Adam of layer l on a side stream beside the Y
     build (and apply, 2) of layer l+1 (``LayerSchedule(pipeline=...)``).
+    partition: SMs of a green-context partition that runs stage 1 of every layer
+    back to back while the rest of the SMs run each layer's stage 2, Adam, Y
+    build and apply (``set_partition``); 0: no partition.
     """
 
     def __init__(self, layers: Sequence[Layer], comm: Optional[Comm] = None, backward=None,
-                 pipeline: int = 0):
+                 pipeline: int = 0, partition: int = 0):
         self.layers = list(layers)
         self.comm = comm
         arr = (C.c_void_p * len(self.layers))(*[l.handle for l in self.layers])
@@ -691,6 +694,18 @@ class Schedule:
             self.set_backward(backward)
         if pipeline:
             lib.schedule_set_pipeline(self._h, int(pipeline))
+        self.partition = (0, 0)
+        if partition:
+            self.set_partition(partition)
+
+    def set_partition(self, compress_sms: int):
+        """Split the SMs into a stage-1 partition of ``compress_sms`` (rounded up
+        by the driver) and an update partition (lsp_schedule_set_partition);
+        returns the provisioned (compress, update) SM counts."""
+        c, u = C.c_int(), C.c_int()
+        lib.schedule_set_partition(self._h, int(compress_sms), C.byref(c), C.byref(u))
+        self.partition = (c.value, u.value)
+        return self.partition
 
     def set_backward(self, backward):
         torch = _torch()

@@ -337,3 +337,75 @@ def test_native_schedule_nonfinite_layer_skipped(cuda, comm, mode):
     for li in range(L):
         if li != bad:
             lb[li].check()
+
+
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_native_partition_bitwise_and_capture(cuda, comm, with_comm):
+    """lsp_schedule_set_partition: stage 1 of every layer on a green-context
+    partition of the SMs, the rest of each layer's chain on the other; the
+    persistent grids are sized per partition.  Same kernels on the same data:
+    weights bitwise equal to the serial schedule, eager and as graph replays."""
+    c = comm if with_comm else None
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    lc, wc, ac = _build()
+    for li in range(L):
+        for acts in (aa, ab, ac):
+            _backward(acts)(li)
+    sa = LayerSchedule(la, 1e-3, comm=c)
+    sb = lsp.Schedule(lb, comm=c, partition=40)
+    sc = lsp.Schedule(lc, comm=c, partition=64)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    for s, want in ((sb, 40), (sc, 64)):
+        pc, pu = s.partition
+        assert pc >= want and pc % 8 == 0 and pu > 0 and pc + pu <= nsm
+    for _ in range(4):
+        sa.step()
+        sb.step(1e-3)
+    sc.step(1e-3)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sc.step(1e-3)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for x, y, z in zip(wa, wb, wc):
+        assert torch.equal(x, y) and torch.equal(x, z)
+    # the budgets the step swapped in are restored afterwards
+    sb.set_partition(0)
+    assert sb.partition == (0, 0)
+    sb.step(1e-3)
+    sa.step()
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+
+
+def test_native_partition_nonfinite_and_exclusive(cuda):
+    la, wa, aa = _build()
+    lb, wb, ab = _build()
+    for li in range(L):
+        _backward(aa)(li)
+        _backward(ab)(li)
+    bad = 2
+    ab[bad][0][2][0, 0] = float("inf")
+    w0 = [w.clone() for w in wb]
+    sa = LayerSchedule(la, 1e-3)
+    sb = lsp.Schedule(lb, partition=48)
+    sa.step()
+    sb.step(1e-3)
+    torch.cuda.synchronize()
+    per = len(SHAPES)
+    for li in range(L):
+        for i in range(per):
+            k = li * per + i
+            assert torch.equal(wb[k], w0[k] if li == bad else wa[k])
+    with pytest.raises(lsp.NumericError):
+        lb[bad].check()
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    with pytest.raises(lsp.LspError):
+        sb.set_partition(nsm)  # nothing left for the update partition
+    s = lsp.Schedule(la, pipeline=1, partition=48)
+    with pytest.raises(lsp.InvalidArgument):
+        s.step(1e-3)

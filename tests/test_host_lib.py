@@ -129,3 +129,8 @@ def test_schedule_rejects_bad_args():
 def test_schedule_set_pipeline_rejects_bad_args():
     with pytest.raises(lsp.InvalidArgument):
         lsp.lib.schedule_set_pipeline(None, 1)
+
+
+def test_schedule_set_partition_rejects_bad_args():
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.schedule_set_partition(None, 64, None, None)
