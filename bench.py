@@ -43,13 +43,17 @@ CONFIGS = {
            [(4096, 4096, 4), (4096, 11008, 2), (11008, 4096, 1)], 1024, 4, "f32", "f32"),
     "c4-bf16": ("Llama-7B 32-layer stack, d=1024, r=4, bf16 (BASELINE configs[3])", 32,
                 [(4096, 4096, 4), (4096, 11008, 2), (11008, 4096, 1)], 1024, 4, "bf16", "bf16"),
+    # the reference's own precision: fp64 G, W, projectors, S/M/V (not a BASELINE
+    # config; the device path is bit-exact to the reference's Adam in fp64)
+    "c4-f64": ("Llama-7B 32-layer stack, d=1024, r=4, fp64 (the reference's precision)", 32,
+               [(4096, 4096, 4), (4096, 11008, 2), (11008, 4096, 1)], 1024, 4, "f64", "f64"),
 }
 BYTES = {"f32": 4, "bf16": 2, "f64": 8}
 
 
 def dtype_label(gdt, wdt):
     """Arithmetic type of the step's big streams (G read, W read-modify-write);
-    S/M/V and every accumulation are fp32 regardless."""
+    S/M/V and every accumulation are fp32 (fp64 for the f64 config)."""
     return gdt if gdt == wdt else f"g={gdt},w={wdt}"
 
 
@@ -141,20 +145,21 @@ def matrices(L, shapes):
 
 
 def b_alg(m, n, d, r, bg, bw, bv=4):
-    """algorithmic HBM bytes of one matrix step."""
-    return m * n * (bg + 2 * bw) + 24 * d * d + 2 * (m + n) * r * (4 + bv)
+    """algorithmic HBM bytes of one matrix step (bv = bytes of the
+    compute type: projector values and the S, M, V, delta state, 24 d^2 in fp32)."""
+    return m * n * (bg + 2 * bw) + 6 * bv * d * d + 2 * (m + n) * r * (4 + bv)
 
 
 def apply_bytes(m, n, d, r, bw, bv=4):
     """Algorithmic bytes of one decompress-and-apply launch: W read+write once,
     delta^T read once, CSR (pos, val) of P and Q read once."""
-    return 2 * m * n * bw + 4 * d * d + (m + n) * r * (4 + bv)
+    return 2 * m * n * bw + bv * d * d + (m + n) * r * (4 + bv)
 
 
 def compress_bytes(m, n, d, r, bg, bv=4):
     """Algorithmic bytes of one compress (stage 1 + 2): G read once, S written once,
     projector entries read once."""
-    return m * n * bg + 4 * d * d + (m + n) * r * (4 + bv)
+    return m * n * bg + bv * d * d + (m + n) * r * (4 + bv)
 
 
 # ---------------------------------------------------------------------------
@@ -398,7 +403,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     desc, L, shapes, d, r, gdt, wdt = workload(args)
-    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f64": torch.float64}
+    compute = "f64" if gdt == "f64" else "f32"
     mats = matrices(L, shapes)
 
     # ---- setup (not timed): one lsp.Layer (grouped launches) per model layer ----
@@ -412,8 +418,8 @@ def run_ours(args):
             # projectors: the reference trainer seed path, identical on every rank
             pp, pv = lsp.init_sparse(m, d, r, lsp.derive_seed(args.seed, KINIT, 2 * idx))
             qp, qv = lsp.init_sparse(n, d, r, lsp.derive_seed(args.seed, KINIT, 2 * idx + 1))
-            pair = lsp.DevicePair(lsp.DeviceProjector(m, d, r, pp, pv),
-                                  lsp.DeviceProjector(n, d, r, qp, qv))
+            pair = lsp.DevicePair(lsp.DeviceProjector(m, d, r, pp, pv, compute),
+                                  lsp.DeviceProjector(n, d, r, qp, qv, compute))
             gen.manual_seed(lsp.derive_seed(args.seed, 0x6, idx * world + rank))
             g = torch.randn(m, n, device=dev, generator=gen).to(tdt[gdt])
             w = (0.02 * torch.randn(m, n, device=dev, generator=gen)).to(tdt[wdt])
@@ -523,12 +529,13 @@ def run_ours(args):
     bg, bw = BYTES[gdt], BYTES[wdt]
     grad_bytes = sum(it["m"] * it["n"] for it in items) * bg
     value = world * grad_bytes / (ms * 1e-3) / 1e9
-    balg = sum(b_alg(it["m"], it["n"], d, r, bg, bw) for it in items)
+    bv = BYTES[compute]
+    balg = sum(b_alg(it["m"], it["n"], d, r, bg, bw, bv) for it in items)
     peak, peak_src = measured_peaks()
     # dominant kernel: the grouped decompress-and-apply (one k_decompress_band
     # launch per layer, bracketed alone by the "apply" events)
-    app_bytes = sum(apply_bytes(it["m"], it["n"], d, r, bw) for it in items) / L
-    comp_bytes = sum(compress_bytes(it["m"], it["n"], d, r, bg) for it in items) / L
+    app_bytes = sum(apply_bytes(it["m"], it["n"], d, r, bw, bv) for it in items) / L
+    comp_bytes = sum(compress_bytes(it["m"], it["n"], d, r, bg, bv) for it in items) / L
     app_avg = float(np.mean(app_ms))
     comp_avg = float(np.mean(comp_ms))
     app_ach = app_bytes / (app_avg * 1e-3) / 1e9
@@ -561,9 +568,11 @@ def run_ours(args):
                    "step_hbm_bytes_alg": balg,
                    "step_hbm_frac_of_measured": balg / (ms * 1e-3) / 1e9 / peak,
                    "step_hbm_frac_of_8TBs": balg / (ms * 1e-3) / 1e9 / 8000.0},
-        "roofline": {"kernel": "k_apply_y (grouped streaming decompress-and-apply W -= lr P Y, "
-                               "1 launch per layer; Y = delta Q^T built by k_build_y_tile just "
-                               "before, timed separately as build_ms)",
+        "roofline": {"kernel": ("k_apply_y (grouped streaming decompress-and-apply W -= lr P Y, "
+                                "1 launch per layer; Y = delta Q^T built by k_build_y_tile just "
+                                "before, timed separately as build_ms)") if compute == "f32" else
+                               ("k_decompress_tma (grouped fp64 decompress-and-apply, Y band "
+                                "built in-kernel from delta^T, 1 launch per layer)"),
                      "bound": "hbm", "achieved": app_ach, "peak": peak, "unit": "GB/s",
                      "frac": app_ach / peak, "traffic": traffic,
                      "traffic_source": (f"{traffic_src}: ncu --set full dram__bytes_read.sum + "
@@ -830,7 +839,8 @@ def e2e(args, items, layers, order, world, dist, torch, dev, bg, comm=None):
     gbytes = sum(it["m"] * it["n"] for it in items) * bg
     return {"value": world * gbytes / dt / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": int(gbytes),
-            "d2h_bytes_per_step": int(sum(l.s_buffer().numel() * 4 for l in layers)),
+            "d2h_bytes_per_step": int(sum(l.s_buffer().numel() * l.s_buffer().element_size()
+                                          for l in layers)),
             "ms_per_step": dt * 1e3, "steps": steps,
             "note": "wall clock incl. H2D of every G from pinned host memory and D2H of every S"}
 

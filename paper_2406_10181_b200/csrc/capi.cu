@@ -196,29 +196,36 @@ const EntryF* Projector::csc_entries() {
 }
 
 const Projector::PadTable& Projector::csc_padded() {
-  require(compute == LSP_F32, "csc_padded: fp32 projectors only");
   if (!csc_pad) {
     auto t = std::make_unique<PadTable>();
     t->h_ptr.assign(d + 1, 0);
-    std::vector<EntryF> e;
-    std::vector<int32_t> perm;
+    std::vector<int32_t> rows, perm;
     for (int b = 0; b < d; ++b) {
       const int k0 = h_csc_ptr[b], k1 = h_csc_ptr[b + 1];
       for (int k = k0; k < k1; ++k) {
-        e.push_back(EntryF{h_csc_rows[k], static_cast<float>(h_val[h_csc_perm[k]])});
+        rows.push_back(h_csc_rows[k]);
         perm.push_back(h_csc_perm[k]);
       }
       const int cnt = k1 - k0, padded = (cnt + kPadU - 1) / kPadU * kPadU;
       for (int k = cnt; k < padded; ++k) {
-        e.push_back(EntryF{h_csc_rows[k1 - 1], 0.0f});
+        rows.push_back(h_csc_rows[k1 - 1]);
         perm.push_back(-1);
       }
-      t->h_ptr[b + 1] = static_cast<int32_t>(e.size());
+      t->h_ptr[b + 1] = static_cast<int32_t>(rows.size());
     }
-    t->count = static_cast<long long>(e.size());
+    t->count = static_cast<long long>(rows.size());
     upload(t->ptr, t->h_ptr.data(), t->h_ptr.size() * sizeof(int32_t));
-    upload(t->ent, e.data(), e.size() * sizeof(EntryF));
-    upload(t->perm, perm.data(), perm.size() * sizeof(int32_t));
+    LSP_DISPATCH_ACC(compute, T, {
+      using E = typename EntryOf<T>::type;
+      std::vector<E> e(rows.size());
+      for (size_t k = 0; k < rows.size(); ++k) {
+        e[k] = E{};
+        e[k].off = rows[k];
+        e[k].val = perm[k] >= 0 ? static_cast<T>(h_val[perm[k]]) : T(0);
+      }
+      upload(t->ent, e.data(), std::max<size_t>(e.size(), 1) * sizeof(E));
+    })
+    upload(t->perm, perm.data(), std::max<size_t>(perm.size(), 1) * sizeof(int32_t));
     csc_pad = std::move(t);
     launch_refresh_values(*this, nullptr);  // current device values
     LSP_CUDA(cudaDeviceSynchronize());

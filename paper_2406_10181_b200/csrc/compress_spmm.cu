@@ -1,6 +1,7 @@
 // Compress stage 1, gather form: Z^T = G^T P (n x d) for fp32 accumulation of
-// fp32 / bf16 G (reference: the G^T P half of S = P^T G Q,
-// proj/src/projector.cpp:119-168; compress :163-168).
+// fp32 / bf16 G, and fp64 accumulation of fp64 G (the reference's precision)
+// (reference: the G^T P half of S = P^T G Q, proj/src/projector.cpp:119-168;
+// compress :163-168).
 //
 // Z[b][:] = sum_{i in CSC_P(b)} p(i,b) * G[i][:] is a sparse x dense product
 // whose sparse factor has ~m*r/d entries per output row.  One warp computes
@@ -39,8 +40,8 @@ struct PMat {
   const void* g;
   long long ldg;
   const int* ptr;       // CSC_P offsets [d + 1]
-  const EntryF* ent;    // CSC_P entries {row, value}
-  float* zt;
+  const void* ent;      // CSC_P entries {row, value}: EntryF (fp32) / EntryD (fp64)
+  void* zt;
   int ldz, n, ntiles;
   long long item_end;
 };
@@ -63,6 +64,14 @@ struct Vec<float> {
   }
 };
 template <>
+struct Vec<double> {
+  static constexpr int CPL = 2;
+  __device__ __forceinline__ static void load(const void* p, double (&g)[2]) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    g[0] = v.x, g[1] = v.y;
+  }
+};
+template <>
 struct Vec<bf16> {
   static constexpr int CPL = 8;
   __device__ __forceinline__ static void load(const void* p, float (&g)[8]) {
@@ -76,14 +85,34 @@ struct Vec<bf16> {
   }
 };
 
-template <typename Tin, int U>
+// entry words as loaded: {row, fp32 value bits} / {row, pad, fp64 value}
+template <typename Tacc>
+struct EntW;
+template <>
+struct EntW<float> {
+  using E = EntryF;
+  using W = uint2;
+  __device__ __forceinline__ static float val(const W& w) { return __uint_as_float(w.y); }
+};
+template <>
+struct EntW<double> {
+  using E = EntryD;
+  using W = uint4;
+  __device__ __forceinline__ static double val(const W& w) {
+    return __hiloint2double(static_cast<int>(w.w), static_cast<int>(w.z));
+  }
+};
+
+template <typename Tin, typename Tacc, int U>
 __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __grid_constant__ PArgs A) {
   constexpr int CPL = Vec<Tin>::CPL;
   constexpr int CT = 32 * CPL;  // columns per tile
   constexpr int LDS = CT + 1;   // padded row of the transpose buffer
+  using E = typename EntW<Tacc>::E;
+  using EW = typename EntW<Tacc>::W;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* zs = reinterpret_cast<float*>(smem_raw);                        // [2][kBG][LDS]
-  unsigned char* ebuf = smem_raw + 2 * kBG * LDS * sizeof(float);        // [2][A.ebuf_bytes]
+  Tacc* zs = reinterpret_cast<Tacc*>(smem_raw);                         // [2][kBG][LDS]
+  unsigned char* ebuf = smem_raw + 2 * kBG * LDS * sizeof(Tacc);        // [2][A.ebuf_bytes]
   unsigned long long* ebar = reinterpret_cast<unsigned long long*>(ebuf + 2 * A.ebuf_bytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rot = lane / (32 / CPL);  // store rotation: conflict-free transposed writes
@@ -106,9 +135,9 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
     const It t = item_at(item);
     const PMat& M = A.mat[t.mi];
     const int ehi = __ldg(M.ptr + min(t.b0 + kBG, A.d));
-    const unsigned bytes = static_cast<unsigned>(round_up16((ehi - t.elo) * 8));
+    const unsigned bytes = static_cast<unsigned>(round_up16((ehi - t.elo) * static_cast<int>(sizeof(E))));
     mbar_arrive_expect_tx(ebar + b, bytes);
-    if (bytes) bulk_load(ebuf + b * A.ebuf_bytes, M.ent + t.elo, bytes, ebar + b);
+    if (bytes) bulk_load(ebuf + b * A.ebuf_bytes, static_cast<const E*>(M.ent) + t.elo, bytes, ebar + b);
   };
 
   if (threadIdx.x == 0) {
@@ -133,8 +162,8 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
     const unsigned char* gcol = static_cast<const unsigned char*>(M.g) +
                                 (jl < M.n ? jl : 0) * static_cast<int>(sizeof(Tin));
     const unsigned ldgb = static_cast<unsigned>(M.ldg * sizeof(Tin));  // < 4 GiB (host check)
-    const EntryF* es = reinterpret_cast<const EntryF*>(ebuf + buf * A.ebuf_bytes) - t.elo;
-    float* z = zs + buf * kBG * LDS;
+    const E* es = reinterpret_cast<const E*>(ebuf + buf * A.ebuf_bytes) - t.elo;
+    Tacc* z = zs + buf * kBG * LDS;
     mbar_wait(ebar + buf, (k >> 1) & 1);
 
     // This warp's two bins as one stream of U-entry batches (bins are padded
@@ -161,28 +190,28 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
         if (w == x) r = arr[x];
       return r;
     };
-    float acc[CPL];
+    Tacc acc[CPL];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    for (int c = 0; c < CPL; ++c) acc[c] = Tacc(0);
     auto flush = [&](int bb) {
       // z[bb][lane*CPL + c], components rotated per lane group so that the
       // CPL stores of a warp each hit 32 distinct banks
-      float* zr = z + bb * LDS + lane * CPL;
+      Tacc* zr = z + bb * LDS + lane * CPL;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const int cc = (c + rot) % CPL;
-        float v = acc[0];
+        Tacc v = acc[0];
 #pragma unroll
         for (int q = 1; q < CPL; ++q)
           if (cc == q) v = acc[q];
         zr[cc] = v;
       }
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+      for (int c = 0; c < CPL; ++c) acc[c] = Tacc(0);
     };
     // load cursor (bin lb, next batch at lsrc, lleft batches left in the bin)
     int lb = 0, lleft = nb_w[0];
-    const EntryF* lsrc = es + es_w[0];
+    const E* lsrc = es + es_w[0];
     auto load_skip = [&]() {
       while (lleft == 0 && lb < NBW - 1) {
         ++lb;
@@ -191,21 +220,21 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
       }
     };
     load_skip();
-    uint2 ena[U], enb[U];
-    float ga[U][CPL], gb[U][CPL];
-    auto load = [&](uint2 (&en)[U], float (&g)[U][CPL]) {
-      const EntryF* src = lsrc;
+    EW ena[U], enb[U];
+    Tacc ga[U][CPL], gb[U][CPL];
+    auto load = [&](EW (&en)[U], Tacc (&g)[U][CPL]) {
+      const E* src = lsrc;
       lsrc += U;
       if (--lleft == 0) load_skip();
 #pragma unroll
-      for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const uint2*>(src + u);
+      for (int u = 0; u < U; ++u) en[u] = *reinterpret_cast<const EW*>(src + u);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         Vec<Tin>::load(gcol + static_cast<unsigned long long>(en[u].x * ldgb), g[u]);
     };
     // consume cursor: bin cb, cleft batches left in it; completed bins flushed
     int cb = 0, cleft = nb_w[0];
-    auto consume = [&](const uint2 (&en)[U], const float (&g)[U][CPL]) {
+    auto consume = [&](const EW (&en)[U], const Tacc (&g)[U][CPL]) {
       while (cleft == 0 && cb < NBW - 1) {
         flush(warp + cb * kSWarps);
         ++cb;
@@ -214,14 +243,19 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
       --cleft;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        // packed FFMA2: two IEEE fmas per instruction, same per-column chain
-        const float p = __uint_as_float(en[u].y);
-        const float2 pp = make_float2(p, p);
+        const Tacc p = EntW<Tacc>::val(en[u]);
+        if constexpr (sizeof(Tacc) == 4) {
+          // packed FFMA2: two IEEE fmas per instruction, same per-column chain
+          const float2 pp = make_float2(p, p);
 #pragma unroll
-        for (int c = 0; c < CPL; c += 2) {
-          const float2 r = __ffma2_rn(pp, make_float2(g[u][c], g[u][c + 1]), make_float2(acc[c], acc[c + 1]));
-          acc[c] = r.x;
-          acc[c + 1] = r.y;
+          for (int c = 0; c < CPL; c += 2) {
+            const float2 r = __ffma2_rn(pp, make_float2(g[u][c], g[u][c + 1]), make_float2(acc[c], acc[c + 1]));
+            acc[c] = r.x;
+            acc[c + 1] = r.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[c] = __fma_rn(p, g[u][c], acc[c]);
         }
       }
     };
@@ -250,15 +284,17 @@ __global__ void __launch_bounds__(kSThreads, kSCtas) k_compress_spmm(const __gri
 #pragma unroll
       for (int h = 0; h < kBG / 32; ++h)
         if (t.b0 + h * 32 + lane < A.d)
-          M.zt[static_cast<long long>(j) * M.ldz + t.b0 + h * 32 + lane] = z[(h * 32 + lane) * LDS + c];
+          static_cast<Tacc*>(M.zt)[static_cast<long long>(j) * M.ldz + t.b0 + h * 32 + lane] =
+              z[(h * 32 + lane) * LDS + c];
     }
     // z[buf] is rewritten two items later, after the next __syncthreads
   }
 }
 
-template <typename Tin>
+template <typename Tin, typename Tacc>
 bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
   constexpr int CPL = Vec<Tin>::CPL;
+  constexpr int ES = static_cast<int>(sizeof(typename EntW<Tacc>::E));
   constexpr int CT = 32 * CPL;
   const Pair& p0 = *jobs[0].pr;
   PArgs A{};
@@ -277,8 +313,8 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
     M.ldg = J.ldg;
     const Projector::PadTable& pt = pr.p->csc_padded();
     M.ptr = pt.ptr.as<int>();
-    M.ent = pt.ent.as<EntryF>();
-    M.zt = static_cast<float*>(J.zt);
+    M.ent = pt.ent.p;
+    M.zt = J.zt;
     M.ldz = pr.ldz();
     M.n = pr.n;
     M.ntiles = ceil_div(pr.n, CT);
@@ -294,10 +330,11 @@ bool spmm_impl(const std::vector<S1Job>& jobs, cudaStream_t st) {
     for (int b0 = 0; b0 < p0.d; b0 += kBG)
       emax = std::max(emax, ptr[std::min(b0 + kBG, p0.d)] - ptr[b0]);
   }
-  A.ebuf_bytes = round_up16(emax * 8 + 16);
-  const int smem = 2 * kBG * (CT + 1) * static_cast<int>(sizeof(float)) + 2 * A.ebuf_bytes + 16;
+  A.ebuf_bytes = round_up16(emax * ES + 16);
+  const int smem = 2 * kBG * (CT + 1) * static_cast<int>(sizeof(Tacc)) + 2 * A.ebuf_bytes + 16;
   if (smem > 227 * 1024) return false;
-  auto kern = k_compress_spmm<Tin, Projector::kPadU>;  // U = pad unit
+  // U = pad unit (fp32); fp64 keeps half the loads in flight (register budget)
+  auto kern = k_compress_spmm<Tin, Tacc, sizeof(Tacc) == 4 ? Projector::kPadU : Projector::kPadU / 2>;
   LSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = static_cast<int>(std::min<long long>(total, kSCtas * sm_budget(kBudgetCompress)));
   kern<<<grid, kSThreads, smem, st>>>(A);
@@ -317,10 +354,11 @@ bool launch_compress_spmm_group(const std::vector<S1Job>& jobs, lsp_dtype gdt, c
   const char* gen = std::getenv("LSP_COMPRESS_GENERIC");
   if (gen && gen[0] == '1') return false;
   const Pair& p0 = *jobs[0].pr;
-  if (p0.compute != LSP_F32 || (gdt != LSP_F32 && gdt != LSP_BF16)) return false;
   const char* env = std::getenv("LSP_COMPRESS_SPMM");
   if (env && env[0] == '0') return false;
-  return gdt == LSP_F32 ? spmm_impl<float>(jobs, st) : spmm_impl<bf16>(jobs, st);
+  if (p0.compute == LSP_F64) return gdt == LSP_F64 && spmm_impl<double, double>(jobs, st);
+  if (p0.compute != LSP_F32 || (gdt != LSP_F32 && gdt != LSP_BF16)) return false;
+  return gdt == LSP_F32 ? spmm_impl<float, float>(jobs, st) : spmm_impl<bf16, float>(jobs, st);
 }
 
 }  // namespace lspb

@@ -111,7 +111,8 @@ struct Projector {
   const EntryF* csc_entries();
   DevBuf csc_ent;
   // CSC entries with every bin padded to a multiple of kPadU entries (pads:
-  // the bin's last row, value 0, perm -1) for the gather-form compress.
+  // the bin's last row, value 0, perm -1) for the gather-form compress;
+  // EntryF for fp32 projectors, EntryD for fp64.
   static constexpr int kPadU = 8;
   struct PadTable {
     DevBuf ptr, ent, perm;

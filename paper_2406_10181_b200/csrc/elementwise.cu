@@ -252,12 +252,13 @@ void launch_refresh_values(const Projector& p, cudaStream_t st) {
                                                                  p.val.as<T>(), ct->ent.as<E>());
       after_launch("refresh_chunks");
     }
+    if (p.csc_pad && p.csc_pad->count) {
+      using E = typename EntryOf<T>::type;
+      k_gather_entry_values<E, T><<<grid_for(p.csc_pad->count), 256, 0, st>>>(
+          p.csc_pad->count, p.csc_pad->perm.as<int>(), p.val.as<T>(), p.csc_pad->ent.as<E>());
+      after_launch("refresh_csc_padded");
+    }
     if constexpr (sizeof(T) == 4) {
-      if (p.csc_pad && p.csc_pad->count) {
-        k_gather_entry_values<EntryF, T><<<grid_for(p.csc_pad->count), 256, 0, st>>>(
-            p.csc_pad->count, p.csc_pad->perm.as<int>(), p.val.as<T>(), p.csc_pad->ent.as<EntryF>());
-        after_launch("refresh_csc_padded");
-      }
       if (p.csc_ent.p && nnz) {
         k_gather_entry_values<EntryF, T><<<grid_for(nnz), 256, 0, st>>>(
             nnz, p.csc_perm.as<int>(), p.val.as<T>(), p.csc_ent.as<EntryF>());

@@ -511,6 +511,39 @@ def test_compress_paths_agree(cuda, port, gdt, pin, monkeypatch):
         assert rel(host(outs[0]), port.compress(P, Q, g)) < 1e-5
 
 
+def test_compress_paths_agree_fp64(cuda, port, monkeypatch):
+    """fp64 (the reference's precision): the gather-form stage 1 and the CSC-walk
+    stage 1 are bitwise identical, and match the oracle at 1e-12; random and
+    skewed projectors, ragged shapes, d not a multiple of 32; then a value
+    refresh through set_values."""
+    cases = []
+    for (m, n, d, r) in [(777, 1000, 64, 4), (1300, 4100, 128, 4), (4096, 96, 1024, 4),
+                         (513, 258, 100, 3), (2000, 300, 2048, 8), (300, 8192, 64, 2)]:
+        P, Q, _ = make(port, m, n, d, r, m + n)
+        cases.append((P, Q))
+    cases.append((_skewed(1500, 96, 4, 1, 1), port.init_sparse(704, 96, 4, 5)))
+    for P, Q in cases:
+        g = np.random.default_rng(P.n_rows).standard_normal((P.n_rows, Q.n_rows))
+        outs = []
+        for spmm in ("1", "0"):
+            monkeypatch.setenv("LSP_COMPRESS_SPMM", spmm)
+            pair = lsp.DevicePair(lsp.DeviceProjector(P.n_rows, P.d, P.r, P.pos, P.val, "f64"),
+                                  lsp.DeviceProjector(Q.n_rows, Q.d, Q.r, Q.pos, Q.val, "f64"))
+            outs.append(pair.compress(dev(g, "f64")).clone())
+        assert torch.equal(outs[0], outs[1])
+        assert rel(host(outs[0]), port.compress(P, Q, g)) < 1e-12
+    monkeypatch.setenv("LSP_COMPRESS_SPMM", "1")
+    P, Q = cases[0]
+    dp = lsp.DeviceProjector(P.n_rows, P.d, P.r, P.pos, P.val, "f64")
+    pair = lsp.DevicePair(dp, lsp.DeviceProjector(Q.n_rows, Q.d, Q.r, Q.pos, Q.val, "f64"))
+    g = np.random.default_rng(9).standard_normal((P.n_rows, Q.n_rows))
+    pair.compress(dev(g, "f64"))  # builds the padded entry table
+    P2 = P.copy()
+    P2.val = np.random.default_rng(3).standard_normal(P.val.shape)
+    dp.set_values(P2.val)
+    assert rel(host(pair.compress(dev(g, "f64"))), port.compress(P2, Q, g)) < 1e-12
+
+
 @pytest.mark.parametrize("spmm", ["1", "0"])
 def test_compress_slots_value_refresh(cuda, port, spmm, monkeypatch):
     """set_values re-derives the slot/overflow tables' and the packed CSC entries'
