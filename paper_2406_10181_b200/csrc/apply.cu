@@ -1135,7 +1135,7 @@ static bool y_eligible(const DecJob& J, lsp_dtype dt, double beta) {
 }
 
 bool decompress_fast_eligible(const DecJob& J, lsp_dtype dt, double beta) {
-  return apply_x_eligible(J, dt, beta) || y_eligible(J, dt, beta);
+  return apply_x_eligible(J, dt, beta) || y_eligible(J, dt, beta) || y64_eligible(J, dt, beta);
 }
 
 bool launch_decompress_group_y(const std::vector<DecJob>& all_jobs, lsp_dtype dt, double alpha,
@@ -1143,6 +1143,10 @@ bool launch_decompress_group_y(const std::vector<DecJob>& all_jobs, lsp_dtype dt
   if (all_jobs.empty() || all_jobs.size() > static_cast<size_t>(kMaxGroup)) return false;
   for (const DecJob& J : all_jobs)
     if (!decompress_fast_eligible(J, dt, beta)) return false;
+  if (all_jobs[0].pr->compute == LSP_F64) {  // fp64 twin of the Y path (apply_f64.cu)
+    launch_y64_group(all_jobs, alpha, beta, skip_flag, st, phase);
+    return true;
+  }
   // n > m matrices go to the row orientation (apply_x.cu), the rest here;
   // every matrix's path depends only on the matrix, never on its group
   std::vector<DecJob> jobs, xjobs;

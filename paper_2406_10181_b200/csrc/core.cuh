@@ -222,6 +222,10 @@ bool launch_decompress_group_tma(const std::vector<DecJob>& jobs, lsp_dtype dt, 
 constexpr int kPhaseBuild = 1, kPhaseApply = 2, kPhaseBoth = 3;
 // Does this matrix go through launch_decompress_group_y (row or column form)?
 bool decompress_fast_eligible(const DecJob& J, lsp_dtype dt, double beta);
+// fp64 Y path (apply_f64.cu): per-matrix eligibility, and the group launch.
+bool y64_eligible(const DecJob& J, lsp_dtype dt, double beta);
+void launch_y64_group(const std::vector<DecJob>& jobs, double alpha, double beta, const int* skip,
+                      cudaStream_t st, int phase);
 // Row-orientation apply (apply_x.cu) for n > m matrices.
 bool apply_x_eligible(const DecJob& J, lsp_dtype dt, double beta);
 void launch_apply_x(const std::vector<DecJob>& jobs, double alpha, double beta,

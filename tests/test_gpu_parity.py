@@ -364,6 +364,35 @@ def test_decompress_y_bitwise_vs_band(cuda, port, monkeypatch):
         assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("shape", [(1000, 1500, 256, 4), (777, 1001, 64, 4), (130, 66, 1024, 4),
+                                   (513, 258, 100, 2), (300, 700, 96, 8)])
+def test_decompress_fp64_y_path(cuda, port, shape, monkeypatch):
+    """fp64 (the reference's precision): the Y-precompute path (apply_f64.cu) on
+    the oracle at 1e-12 -- decompress_apply (W -= lr P delta Q^T) and decompress
+    (out = P delta Q^T) -- and, for r = 4, bitwise equal to the in-kernel Y_band
+    kernel (same arithmetic and summation order); odd n covers the last single
+    column, m not a multiple of the 64-row tile, d up to 1024."""
+    m, n, d, r = shape
+    P, Q, pair = make(port, m, n, d, r, m + n, "f64")
+    delta = np.random.default_rng(d).standard_normal((d, d))
+    w0 = 0.02 * np.random.default_rng(m).standard_normal((m, n))
+    outs = []
+    for band in ("0", "1"):
+        monkeypatch.setenv("LSP_DECOMPRESS_BAND", band)
+        w = dev(w0, "f64")
+        pair.decompress_apply(dev(delta, "f64"), 1e-3, w)
+        outs.append(w)
+        if band == "1" and r != 4:
+            break  # the in-kernel band kernel is r = 4 only
+    monkeypatch.delenv("LSP_DECOMPRESS_BAND")
+    ref = port.decompress_apply(P, Q, delta, 1e-3, w0)
+    assert rel(host(outs[0]) - w0, ref - w0) < 1e-12
+    if r == 4:
+        assert torch.equal(outs[0], outs[1])
+    out = host(pair.decompress(dev(delta, "f64")))
+    assert rel(out, port.decompress(P, Q, delta)) < 1e-12
+
+
 def test_apply_cluster_pair_bitwise(cuda, port, monkeypatch):
     """The 2-CTA cluster apply (LSP_APPLY_PAIR=1: leader-issued multicast W boxes
     and P entries, remote stage release) is bitwise equal to the default apply,
