@@ -616,6 +616,79 @@ __global__ void __launch_bounds__(kS2Threads) k_stage2_f4(const __grid_constant_
   if (A.flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(A.flag, 1);
 }
 
+// fp64 twin of k_stage2_f4 (the reference's precision): 16-byte double2 chunks,
+// kS2V2 per thread (d = 1024: the whole row), the same per-element fma chain in
+// CSC entry order, the non-finite latch fused.
+struct S2MatD {
+  const int* ptr;
+  const int* row;
+  const double* val;
+  const double* zt;
+  int ldz;
+  double* s_t;
+};
+struct S2ArgsD {
+  S2MatD mat[kMaxGroup];
+  int count;
+  int d;
+  int* flag;
+};
+constexpr int kS2V2 = 4;
+__global__ void __launch_bounds__(kS2Threads) k_stage2_d2(const __grid_constant__ S2ArgsD A) {
+  const S2MatD& M = A.mat[blockIdx.y];
+  const int b = blockIdx.x, d = A.d;
+  const int e0 = __ldg(M.ptr + b), e1 = __ldg(M.ptr + b + 1);
+  bool bad = false;
+  for (int a_base = 2 * threadIdx.x; a_base < d; a_base += 2 * kS2Threads * kS2V2) {
+    double2 acc[kS2V2];
+    bool ok[kS2V2];
+#pragma unroll
+    for (int c = 0; c < kS2V2; ++c) {
+      acc[c] = make_double2(0.0, 0.0);
+      ok[c] = a_base + c * 2 * kS2Threads < d;
+    }
+    int e = e0;
+    for (; e + 2 <= e1; e += 2) {
+      double2 z[2][kS2V2];
+      double q[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        q[u] = __ldg(M.val + e + u);
+        const double* zr = M.zt + static_cast<long long>(__ldg(M.row + e + u)) * M.ldz + a_base;
+#pragma unroll
+        for (int c = 0; c < kS2V2; ++c)
+          z[u][c] = ok[c] ? __ldg(reinterpret_cast<const double2*>(zr + c * 2 * kS2Threads))
+                          : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int c = 0; c < kS2V2; ++c) {
+          acc[c].x = fma(q[u], z[u][c].x, acc[c].x);
+          acc[c].y = fma(q[u], z[u][c].y, acc[c].y);
+        }
+    }
+    for (; e < e1; ++e) {
+      const double q = __ldg(M.val + e);
+      const double* zr = M.zt + static_cast<long long>(__ldg(M.row + e)) * M.ldz + a_base;
+#pragma unroll
+      for (int c = 0; c < kS2V2; ++c) {
+        if (!ok[c]) continue;
+        const double2 z = __ldg(reinterpret_cast<const double2*>(zr + c * 2 * kS2Threads));
+        acc[c].x = fma(q, z.x, acc[c].x);
+        acc[c].y = fma(q, z.y, acc[c].y);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kS2V2; ++c) {
+      if (!ok[c]) continue;
+      bad |= !(isfinite(acc[c].x) && isfinite(acc[c].y));
+      *reinterpret_cast<double2*>(M.s_t + static_cast<long long>(b) * d + a_base + c * 2 * kS2Threads) = acc[c];
+    }
+  }
+  if (A.flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(A.flag, 1);
+}
+
 }  // namespace
 
 void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t st) {
@@ -644,6 +717,26 @@ void launch_stage2_group(const std::vector<S1Job>& jobs, int* flag, cudaStream_t
     }
     k_stage2_f4<<<dim3(d, A.count), kS2Threads, 0, st>>>(A);
     after_launch("stage2");
+    return;
+  }
+  bool fast64 = p0.compute == LSP_F64 && d % 2 == 0;
+  for (const S1Job& J : jobs)
+    fast64 = fast64 && J.pr->ldz() % 2 == 0 && reinterpret_cast<uintptr_t>(J.zt) % 16 == 0 &&
+             reinterpret_cast<uintptr_t>(J.s_t) % 16 == 0;
+  if (fast64) {
+    S2ArgsD A{};
+    A.count = static_cast<int>(jobs.size());
+    A.d = d;
+    A.flag = flag;
+    for (size_t i = 0; i < jobs.size(); ++i) {  // reverse: the last-written Z^T first
+      const size_t ji = jobs.size() - 1 - i;
+      const Projector& Q = *jobs[ji].pr->q;
+      A.mat[i] = S2MatD{Q.csc_ptr.as<int>(), Q.csc_row.as<int>(), Q.csc_val.as<double>(),
+                        static_cast<const double*>(jobs[ji].zt), jobs[ji].pr->ldz(),
+                        static_cast<double*>(jobs[ji].s_t)};
+    }
+    k_stage2_d2<<<dim3(d, A.count), kS2Threads, 0, st>>>(A);
+    after_launch("stage2_d2");
     return;
   }
   for (const S1Job& J : jobs) {
