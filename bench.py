@@ -614,7 +614,7 @@ def run_ours(args):
         line["fit"] = fit_leg(args, items, L, shapes, d, r, lsp, torch, dev)
         line["fit"]["ms_per_step_incl_fit"] = ms + line["fit"]["amortized_ms_per_step"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr)
+        cb, _ = cpu_baseline(desc, L, shapes, d, r, gdt, args.lr, reps=5)
         line["cpu_baseline"] = cb
     if not args.no_e2e:
         line["e2e"] = e2e(args, items, layers, order, world, dist, torch, dev, bg, comm)
