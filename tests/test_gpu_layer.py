@@ -22,21 +22,26 @@ def make_layer(d=64, r=4, compute="f32", shapes=SHAPES, seed=3):
     return pairs
 
 
-def test_layer_step_matches_per_matrix_bitwise(cuda):
+@pytest.mark.parametrize("compute", ["f32", "f64"])
+def test_layer_step_matches_per_matrix_bitwise(cuda, compute):
+    """The grouped layer launches (fp32: gather compress + Y path; fp64: the
+    fp64 gather compress, grouped fp64 stage 2 and the fp64 Y path) give
+    exactly the per-matrix results."""
     torch.manual_seed(0)
-    pairs = make_layer()
+    tdt = torch.float32 if compute == "f32" else torch.float64
+    pairs = make_layer(compute=compute)
     layer = lsp.Layer(pairs)
-    gs = [torch.randn(p.m, p.n, device="cuda") for p in pairs]
-    ws = [0.02 * torch.randn(p.m, p.n, device="cuda") for p in pairs]
+    gs = [torch.randn(p.m, p.n, device="cuda", dtype=tdt) for p in pairs]
+    ws = [0.02 * torch.randn(p.m, p.n, device="cuda", dtype=tdt) for p in pairs]
     ws_ref = [w.clone() for w in ws]
     for i, p in enumerate(pairs):
         layer.bind(i, gs[i], ws[i])
-    adams = [lsp.AdamState(p.d) for p in pairs]
+    adams = [lsp.AdamState(p.d, compute=compute) for p in pairs]
     for it in range(3):
         layer.step(1e-3)
         s_refs = []
         for i, p in enumerate(pairs):
-            s_t = torch.empty(p.d, p.d, device="cuda")
+            s_t = torch.empty(p.d, p.d, device="cuda", dtype=tdt)
             lsp.step(p, adams[i], gs[i], ws_ref[i], 1e-3, s_out=s_t)
             s_refs.append(s_t)
         torch.cuda.synchronize()
@@ -104,3 +109,37 @@ def test_layer_rejects_mixed_d(cuda):
     b = lsp.DevicePair(lsp.DeviceProjector.random(64, 32, 2, 3), lsp.DeviceProjector.random(64, 32, 2, 4))
     with pytest.raises(lsp.InvalidArgument):
         lsp.Layer([a, b])
+
+
+@pytest.mark.parametrize("mode", ["serial", "pipeline", "partition"])
+def test_fp64_layers_native_schedule_bitwise(cuda, mode):
+    """fp64 layers through the native schedule (split compress and apply phases
+    in the pipelined order, green-context partition): weights bitwise those of
+    the Python serial schedule."""
+    from paper_2406_10181_b200.schedule import LayerSchedule
+
+    def build():
+        torch.manual_seed(7)
+        layers, ws = [], []
+        for li in range(3):
+            pairs = make_layer(compute="f64", seed=11 + li)
+            lay = lsp.Layer(pairs)
+            for i, p in enumerate(pairs):
+                g = torch.randn(p.m, p.n, device="cuda", dtype=torch.float64)
+                w = 0.02 * torch.randn(p.m, p.n, device="cuda", dtype=torch.float64)
+                lay.bind(i, g, w)
+                ws.append(w)
+            layers.append(lay)
+        return layers, ws
+
+    la, wa = build()
+    lb, wb = build()
+    sa = LayerSchedule(la, 1e-3)
+    sb = lsp.Schedule(lb, pipeline=2 if mode == "pipeline" else 0,
+                      partition=48 if mode == "partition" else 0)
+    for _ in range(3):
+        sa.step()
+        sb.step(1e-3)
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
