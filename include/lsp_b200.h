@@ -254,6 +254,17 @@ int lsp_layer_compress(lsp_layer_t layer, lsp_stream_t stream);
  * Replaces: right_mul then leftT_mul, proj/src/projector.cpp:119-168. */
 int lsp_layer_compress_prepare(lsp_layer_t layer, lsp_stream_t stream);
 int lsp_layer_compress_finish(lsp_layer_t layer, lsp_stream_t stream);
+/* Single-rank forms (no S exchange between compress and Adam): compress (or
+ * its stage 2) with the layer's Adam fused into the stage-2 epilogue, i.e.
+ * lsp_layer_compress + lsp_layer_adam(check 0) (resp. _compress_finish +
+ * _adam) in one launch fewer, bitwise the same S, delta, moments and step.
+ * The moments live in a ping-pong pair flipped by the launch's last CTA, only
+ * when the layer's S was finite (a non-finite layer keeps its moments and step
+ * and latches the flag, as lsp_layer_adam would skip).  Groups the fused
+ * kernel does not cover (fp64, d % 4 != 0, LSP_FUSE_ADAM=0) run the unfused
+ * pair.  Replaces: compress + adam_step, proj/src/trainer.cpp:186-189. */
+int lsp_layer_compress_adam(lsp_layer_t layer, lsp_stream_t stream);
+int lsp_layer_compress_finish_adam(lsp_layer_t layer, lsp_stream_t stream);
 /* Adam on the layer's S^T (optionally re-checking finiteness, e.g. after an
  * all-reduce) and W_i -= lr * P_i delta_i Q_i^T; skipped if the flag is set. */
 int lsp_layer_update(lsp_layer_t layer, double lr, int check_finite, lsp_stream_t stream);

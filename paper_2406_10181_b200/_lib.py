@@ -121,6 +121,8 @@ _SIGS = {
     "lsp_layer_compress": (_i, [_vp, _vp]),
     "lsp_layer_compress_prepare": (_i, [_vp, _vp]),
     "lsp_layer_compress_finish": (_i, [_vp, _vp]),
+    "lsp_layer_compress_adam": (_i, [_vp, _vp]),
+    "lsp_layer_compress_finish_adam": (_i, [_vp, _vp]),
     "lsp_layer_update": (_i, [_vp, _d, _i, _vp]),
     "lsp_layer_adam": (_i, [_vp, _i, _vp]),
     "lsp_maybe_update": (_i, [_vp, _vp, _vp, C.c_int64, _i, _vp, _i, _i, _d, _vp, _i,

@@ -157,6 +157,12 @@ struct Adam {
   DevBuf flag;   // int: latched non-finite gradient
   DevBuf dstep;  // int64: step counter, advanced on the device (graph-replay safe)
   DevBuf done;   // unsigned: blocks finished in the current Adam launch
+  // Ping-pong moments (layer state only; empty otherwise): int `cur` on the
+  // device selects (m, v) or (m2, v2).  k_adam updates the current pair in
+  // place; the stage-2 + Adam kernel writes the other pair and its last block
+  // flips `cur` only when the layer's S was finite, so a skipped step leaves
+  // the moments untouched exactly like k_adam's early return.
+  DevBuf m2, v2, cur;
   size_t count() const { return static_cast<size_t>(rows) * cols; }
 };
 
@@ -237,6 +243,11 @@ void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, doub
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st);
 void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st);
+const double2* correction_table(double b1, double b2, long long* cap);
+// Stage 2 with the layer's Adam fused into its epilogue (fp32, ping-pong
+// moments); false (nothing launched) when the group is not eligible.
+bool launch_stage2_adam_group(const std::vector<S1Job>& jobs, const void* s_base, Adam& a,
+                              void* delta, int* flag, cudaStream_t st);
 void launch_check_finite(size_t cnt, const void* x, lsp_dtype dt, int* flag, cudaStream_t st);
 void launch_convert(size_t cnt, const void* src, lsp_dtype sdt, void* dst, lsp_dtype ddt,
                     cudaStream_t st);

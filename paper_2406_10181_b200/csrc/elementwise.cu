@@ -6,26 +6,16 @@
 #include <mutex>
 #include <vector>
 
+#include "adam_math.cuh"
 #include "core.cuh"
 
 namespace lspb {
 
 // ---------------------------------------------------------------------------
-// Subspace Adam (proj/src/subspace_opt.cpp:35-57).  Elementwise, no
-// contraction (explicit _rn ops) so the fp64 path rounds exactly like the
-// reference: m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
-// delta = (m / c1) / (sqrt(v / c2) + eps).
+// Subspace Adam (proj/src/subspace_opt.cpp:35-57): the element update is
+// adam_elem (adam_math.cuh), no contraction.
 // ---------------------------------------------------------------------------
 namespace {
-
-__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
-__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
-__device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
 
 // Subspace Adam.  Every block reads the step counter, computes the bias
 // corrections (1 - b1^t, 1 - b2^t) from a host table filled with std::pow,
@@ -36,8 +26,13 @@ __global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m
                        T* __restrict__ v, T* __restrict__ delta, T b1, T omb1, T b2, T omb2,
                        const double2* __restrict__ table, long long cap, double db1,
                        double db2, T eps, long long* __restrict__ step,
-                       unsigned* __restrict__ done, const int* __restrict__ skip) {
+                       unsigned* __restrict__ done, const int* __restrict__ skip,
+                       T* m1, T* v1, const int* __restrict__ cur) {
   if (skip && *skip) return;  // uniform over the grid: nobody touches the counter
+  if (cur && *cur) {  // ping-pong moments (layer state): the current pair is (m1, v1)
+    m = m1;
+    v = v1;
+  }
   const long long t = *step + 1;
   double2 c;
   if (t <= cap) {
@@ -48,11 +43,7 @@ __global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m
   }
   const T c1 = static_cast<T>(c.x), c2 = static_cast<T>(c.y);
   auto one = [&](T gi, T& mo, T& vo) {  // returns delta; updates the moments in place
-    const T mi = add_(mul_(b1, mo), mul_(omb1, gi));
-    const T vi = add_(mul_(b2, vo), mul_(mul_(omb2, gi), gi));
-    mo = mi;
-    vo = vi;
-    return div_(div_(mi, c1), add_(sqrt_(div_(vi, c2)), eps));
+    return adam_elem(gi, mo, vo, b1, omb1, b2, omb2, c1, c2, eps);
   };
   long long i0 = 0;
   if constexpr (sizeof(T) == 4) {
@@ -158,7 +149,7 @@ int grid_for(long long cnt) {
 }  // namespace
 
 // Bias-correction tables shared by every state with the same betas.
-static const double2* correction_table(double b1, double b2, long long* cap) {
+const double2* correction_table(double b1, double b2, long long* cap) {
   struct Entry {
     double b1, b2;
     DevBuf buf;
@@ -191,7 +182,8 @@ void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, c
     k_adam<T><<<grid_for(cnt), 256, 0, st>>>(
         cnt, static_cast<const T*>(grad), a.m.as<T>(), a.v.as<T>(), static_cast<T*>(delta),
         (T)a.beta1, (T)(1.0 - a.beta1), (T)a.beta2, (T)(1.0 - a.beta2), table, cap, a.beta1,
-        a.beta2, (T)a.eps, a.dstep.as<long long>(), a.done.as<unsigned>(), skip_flag);
+        a.beta2, (T)a.eps, a.dstep.as<long long>(), a.done.as<unsigned>(), skip_flag,
+        a.m2.as<T>(), a.v2.as<T>(), a.cur.as<const int>());
   })
   after_launch("adam");
 }

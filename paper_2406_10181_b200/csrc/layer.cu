@@ -85,6 +85,21 @@ void layer_adam(lsp_layer_s& L, bool check, cudaStream_t st) {
   launch_adam(L.adam, L.s_t.p, L.d_t.p, flag, st);
 }
 
+// Stage 2 and Adam of a layer with no S exchange between them (single rank):
+// one fused launch when eligible (k_stage2_f4<true>), else the unfused pair.
+void layer_stage2_adam(lsp_layer_s& L, cudaStream_t st) {
+  const std::vector<S1Job> jobs = compress_jobs(L);
+  int* flag = L.adam.flag.as<int>();
+  if (launch_stage2_adam_group(jobs, L.s_t.p, L.adam, L.d_t.p, flag, st)) return;
+  launch_stage2_group(jobs, flag, st);
+  launch_adam(L.adam, L.s_t.p, L.d_t.p, flag, st);
+}
+
+void layer_compress_adam(lsp_layer_s& L, cudaStream_t st) {
+  launch_compress_stage1_group(compress_jobs(L), L.binds[0].gdt, st);
+  layer_stage2_adam(L, st);
+}
+
 void layer_apply(lsp_layer_s& L, double lr, cudaStream_t st) {
   check_bound(L);
   int* flag = L.adam.flag.as<int>();
@@ -201,8 +216,14 @@ int lsp_layer_create(int count, const lsp_pair_t* pairs, double beta1, double be
     a.flag.ensure(sizeof(int));
     a.dstep.ensure(sizeof(long long));
     a.done.ensure(sizeof(unsigned));
+    a.m2.ensure(bytes);  // ping-pong pair of the fused stage-2 + Adam (Adam::cur)
+    a.v2.ensure(bytes);
+    a.cur.ensure(sizeof(int));
     LSP_CUDA(cudaMemset(a.m.p, 0, bytes));
     LSP_CUDA(cudaMemset(a.v.p, 0, bytes));
+    LSP_CUDA(cudaMemset(a.m2.p, 0, bytes));
+    LSP_CUDA(cudaMemset(a.v2.p, 0, bytes));
+    LSP_CUDA(cudaMemset(a.cur.p, 0, sizeof(int)));
     LSP_CUDA(cudaMemset(a.flag.p, 0, sizeof(int)));
     LSP_CUDA(cudaMemset(a.dstep.p, 0, sizeof(long long)));
     LSP_CUDA(cudaMemset(a.done.p, 0, sizeof(unsigned)));
@@ -254,6 +275,20 @@ int lsp_layer_compress_finish(lsp_layer_t L, lsp_stream_t stream) {
   return guard_layer([&] {
     require(L != nullptr, "layer_compress_finish: null layer");
     launch_stage2_group(compress_jobs(*L), L->adam.flag.as<int>(), as_stream(stream));
+  });
+}
+
+int lsp_layer_compress_adam(lsp_layer_t L, lsp_stream_t stream) {
+  return guard_layer([&] {
+    require(L != nullptr, "layer_compress_adam: null layer");
+    layer_compress_adam(*L, as_stream(stream));
+  });
+}
+
+int lsp_layer_compress_finish_adam(lsp_layer_t L, lsp_stream_t stream) {
+  return guard_layer([&] {
+    require(L != nullptr, "layer_compress_finish_adam: null layer");
+    layer_stage2_adam(*L, as_stream(stream));
   });
 }
 
@@ -335,8 +370,10 @@ int lsp_layer_adam_get(lsp_layer_t L, int idx, double* m, double* v, int64_t* st
           }
       })
     };
-    fetch(L->adam.m, m);
-    fetch(L->adam.v, v);
+    int cur = 0;
+    LSP_CUDA(cudaMemcpy(&cur, L->adam.cur.p, sizeof(int), cudaMemcpyDeviceToHost));
+    fetch(cur ? L->adam.m2 : L->adam.m, m);
+    fetch(cur ? L->adam.v2 : L->adam.v, v);
     if (step) {
       long long h = 0;
       LSP_CUDA(cudaMemcpy(&h, L->adam.dstep.p, sizeof(h), cudaMemcpyDeviceToHost));

@@ -7,7 +7,8 @@
 //
 //   for layer l in backward order (last first):
 //     [bwd(l) on the caller's stream through the backward callback -> G_l]
-//     compress(l)                       (LSP stream; gated by bwd(l)'s event)
+//     compress(l)                       (LSP stream; gated by bwd(l)'s event;
+//                                        single rank: Adam fused into stage 2)
 //     all-reduce(S_l, mean)             (comm stream, when a communicator is set)
 //     finish(l+1): wait(S_{l+1}) -> Adam -> Y build -> W -= lr P dS Q^T
 //
@@ -74,9 +75,12 @@ int make_stream(cudaStream_t* s) {
 }
 
 // compress(li) on `src`, then (with a communicator) its all-reduce on the comm stream
+// Without a communicator there is no exchange between stage 2 and Adam, so
+// the layer's Adam runs in the stage-2 epilogue (lsp_layer_compress_adam) and
+// finish() skips it.
 int compress_and_reduce(lsp_schedule_s* S, int li, cudaStream_t src) {
+  if (!S->comm) return lsp_layer_compress_adam(S->layers[li], src);
   LCK(lsp_layer_compress(S->layers[li], src));
-  if (!S->comm) return LSP_OK;
   SCK(cudaEventRecord(S->compressed[li], src));
   SCK(cudaStreamWaitEvent(S->comm_stream, S->compressed[li], 0));
   LCK(lsp_layer_allreduce(S->layers[li], S->comm, S->comm_stream));
@@ -86,8 +90,10 @@ int compress_and_reduce(lsp_schedule_s* S, int li, cudaStream_t src) {
 
 // Adam + apply of layer li on `st`, after its all-reduce
 int finish(lsp_schedule_s* S, int li, double lr, cudaStream_t st) {
-  if (S->comm) SCK(cudaStreamWaitEvent(st, S->reduced[li], 0));
-  LCK(lsp_layer_adam(S->layers[li], S->world > 1 ? 1 : 0, st));  // re-check after the reduction
+  if (S->comm) {
+    SCK(cudaStreamWaitEvent(st, S->reduced[li], 0));
+    LCK(lsp_layer_adam(S->layers[li], S->world > 1 ? 1 : 0, st));  // re-check after the reduction
+  }
   LCK(lsp_layer_apply(S->layers[li], lr, st));
   return LSP_OK;
 }
@@ -113,9 +119,13 @@ int step_pipelined(lsp_schedule_s* S, double lr, cudaStream_t main) {
     LCK(lsp_layer_compress_prepare(L, main));
     SCK(cudaEventRecord(S->compressed[li], main));
     SCK(cudaStreamWaitEvent(S->side, S->compressed[li], 0));
-    LCK(lsp_layer_compress_finish(L, S->side));
-    if (S->comm) LCK(lsp_layer_allreduce(L, S->comm, S->side));
-    LCK(lsp_layer_adam(L, S->world > 1 ? 1 : 0, S->side));
+    if (S->comm) {
+      LCK(lsp_layer_compress_finish(L, S->side));
+      LCK(lsp_layer_allreduce(L, S->comm, S->side));
+      LCK(lsp_layer_adam(L, S->world > 1 ? 1 : 0, S->side));
+    } else {
+      LCK(lsp_layer_compress_finish_adam(L, S->side));
+    }
     SCK(cudaEventRecord(S->updated[li], S->side));
     if (prev >= 0) LCK(finish_pipelined(S, prev, li, lr, main));
     prev = li;
@@ -154,9 +164,13 @@ int step_partitioned(lsp_schedule_s* S, double lr, cudaStream_t main) {
       rc = fail(LSP_ECUDA, "schedule: wait on the compress partition failed");
       break;
     }
-    rc = lsp_layer_compress_finish(L, S->pu);
-    if (rc == LSP_OK && S->comm) rc = lsp_layer_allreduce(L, S->comm, S->pu);
-    if (rc == LSP_OK) rc = lsp_layer_adam(L, S->world > 1 ? 1 : 0, S->pu);
+    if (S->comm) {
+      rc = lsp_layer_compress_finish(L, S->pu);
+      if (rc == LSP_OK) rc = lsp_layer_allreduce(L, S->comm, S->pu);
+      if (rc == LSP_OK) rc = lsp_layer_adam(L, S->world > 1 ? 1 : 0, S->pu);
+    } else {
+      rc = lsp_layer_compress_finish_adam(L, S->pu);
+    }
     if (rc == LSP_OK) rc = lsp_layer_apply(L, lr, S->pu);
   }
   lspb::budget_exchange(oc, ou, nullptr, nullptr);

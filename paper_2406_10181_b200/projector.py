@@ -475,6 +475,16 @@ class Layer:
         """Second half of compress(): stage 2 (S^T = Q^T Z^T) and the non-finite latch."""
         lib.layer_compress_finish(self._h, _stream(stream))
 
+    def compress_adam(self, stream=None):
+        """compress() + adam() for a single rank (no S exchange in between): Adam
+        runs in the stage-2 epilogue (lsp_layer_compress_adam), bitwise the
+        unfused pair."""
+        lib.layer_compress_adam(self._h, _stream(stream))
+
+    def compress_finish_adam(self, stream=None):
+        """compress_finish() + adam() in one launch (lsp_layer_compress_finish_adam)."""
+        lib.layer_compress_finish_adam(self._h, _stream(stream))
+
     def update(self, lr: float, check_finite: bool = False, stream=None):
         lib.layer_update(self._h, float(lr), int(bool(check_finite)), _stream(stream))
 

@@ -27,6 +27,11 @@ Anything that exposes ``compress()``, ``s_buffer()``, ``adam(check)`` and
 ``apply(lr)`` can be scheduled: ``paper_2406_10181_b200.Layer`` on the GPU, or a
 CPU stand-in (tests/test_dist_cpu.py runs this exact class over gloo).
 
+Single rank (no ``comm``/``group``): there is no exchange between stage 2 and
+Adam, so layers that offer ``compress_adam`` run Adam in the stage-2 epilogue
+(one launch fewer per layer, bitwise the same results; ``fuse_adam=False``
+keeps the separate Adam launch).
+
 ``pipeline=1|2`` moves stage 2 (``compress_finish``), the all-reduce and Adam of
 layer l onto a side stream beside the Y build (and, 2, the apply) of layer l+1
 (faster for bf16 W).  The library's native twin of this class is
@@ -44,7 +49,8 @@ class LayerSchedule:
     def __init__(self, layers: Sequence, lr: float, group=None,
                  record: Optional[Callable[[str, int, str], None]] = None, streams=None,
                  comm=None, backward: Optional[Callable[[int], None]] = None,
-                 lsp_stream=None, comm_stream=None, pipeline: int = 0):
+                 lsp_stream=None, comm_stream=None, pipeline: int = 0,
+                 fuse_adam: bool = True):
         """layers: in forward order.
         group: a torch.distributed process group or None (single rank).
         comm: a paper_2406_10181_b200.Comm (the library's NCCL communicator);
@@ -66,6 +72,7 @@ class LayerSchedule:
         self.lsp_stream = lsp_stream
         self.comm_stream = comm_stream
         self.pipeline = pipeline
+        self.fuse_adam = fuse_adam
         self._side = None
         self._events = None
         self.world = 1
@@ -75,6 +82,15 @@ class LayerSchedule:
             import torch.distributed as dist
 
             self.world = dist.get_world_size(group)
+
+    def _fused(self, li):
+        """Adam of layer li runs inside its stage 2 (single rank, native layer)."""
+        return (self.fuse_adam and self.world == 1 and self.comm is None
+                and hasattr(self.layers[li], "compress_adam"))
+
+    def _compress(self, li):
+        lay = self.layers[li]
+        lay.compress_adam() if self._fused(li) else lay.compress()
 
     def _rec(self, phase, li, when):
         if self.record is not None:
@@ -127,7 +143,8 @@ class LayerSchedule:
         if work is not None:
             work.wait()
         self._rec("adam", li, "begin")
-        self.layers[li].adam(self.world > 1)  # re-check finiteness after the reduction
+        if not self._fused(li):
+            self.layers[li].adam(self.world > 1)  # re-check finiteness after the reduction
         self._rec("adam", li, "end")
         lay = self.layers[li]
         if hasattr(lay, "apply_prepare"):
@@ -155,7 +172,7 @@ class LayerSchedule:
         pending = None
         for li in self.order():
             self._rec("compress", li, "begin")
-            self.layers[li].compress()
+            self._compress(li)
             self._rec("compress", li, "end")
             work = self._allreduce(li)
             if pending is not None:
@@ -186,7 +203,7 @@ class LayerSchedule:
             with torch.cuda.stream(ls):
                 ls.wait_event(ev["grad"][li])
                 self._rec("compress", li, "begin")
-                self.layers[li].compress()
+                self._compress(li)
                 self._rec("compress", li, "end")
                 work = self._allreduce(li)
                 if pending is not None:
@@ -219,12 +236,14 @@ class LayerSchedule:
             ev["compressed"][li].record(main)
             with torch.cuda.stream(side):
                 side.wait_event(ev["compressed"][li])
-                lay.compress_finish()
+                fused = self._fused(li)
+                lay.compress_finish_adam() if fused else lay.compress_finish()
                 self._rec("compress", li, "end")
                 if self.comm is not None:
                     lay.allreduce(self.comm)
                 self._rec("adam", li, "begin")
-                lay.adam(self.world > 1)
+                if not fused:
+                    lay.adam(self.world > 1)
                 self._rec("adam", li, "end")
                 ev["update"][li].record(side)
             if prev is not None:
@@ -257,7 +276,7 @@ class LayerSchedule:
         for li in self.order():
             with torch.cuda.stream(sc):
                 self._rec("compress", li, "begin")
-                self.layers[li].compress()
+                self._compress(li)
                 self._rec("compress", li, "end")
                 work = self._allreduce(li)
                 e = None
