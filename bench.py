@@ -211,7 +211,7 @@ class Clocks:
 
 
 KERNEL_SOURCES = ("apply.cu", "compress.cu", "compress_spmm.cu", "elementwise.cu", "layer.cu",
-                  "core.cuh", "tma.cuh")
+                  "core.cuh", "tma.cuh", "adam_math.cuh")
 
 
 def kernel_source_hash():
