@@ -815,10 +815,13 @@ def e2e(args, items, layers, order, world, dist, torch, dev, bg, comm=None):
                 nxt = h2d(order[j + 1])
             main.wait_event(e)
             lay = layers[li]
-            lay.compress()
             if comm is not None:
+                lay.compress()
                 lay.allreduce(comm)
-            lay.update(args.lr)
+                lay.update(args.lr)
+            else:  # single rank: Adam in the stage-2 epilogue, as in the timed step
+                lay.compress_adam()
+                lay.apply(args.lr)
             s_host[li].copy_(lay.s_buffer(), non_blocking=True)
         torch.cuda.synchronize()
 

@@ -53,5 +53,6 @@ def test_our_arm_contract(cuda):
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert d["gpu_launches"] >= 5 * 3
+    # per step: stage 1, stage 2 + Adam (fused at one rank), Y build, apply
+    assert d["gpu_launches"] >= 4 * 3
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
