@@ -242,7 +242,9 @@ bool launch_decompress_group_y(const std::vector<DecJob>& jobs, lsp_dtype dt, do
 void launch_decompress_group(const std::vector<DecJob>& jobs, lsp_dtype dt, double alpha,
                              double beta, const int* skip_flag, DevBuf* partials, int* nparts,
                              cudaStream_t st);
-void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st);
+// checked: fused finiteness check of `grad` (ping-pong state only, see Adam::cur)
+void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st,
+                 bool checked = false);
 const double2* correction_table(double b1, double b2, long long* cap);
 // Stage 2 with the layer's Adam fused into its epilogue (fp32, ping-pong
 // moments); false (nothing launched) when the group is not eligible.

@@ -21,18 +21,25 @@ namespace {
 // corrections (1 - b1^t, 1 - b2^t) from a host table filled with std::pow,
 // exactly like the reference (subspace_opt.cpp:44-45), and the last block to
 // finish advances the counter -- so a captured CUDA graph replays correctly.
-template <typename T>
-__global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m,
-                       T* __restrict__ v, T* __restrict__ delta, T b1, T omb1, T b2, T omb2,
-                       const double2* __restrict__ table, long long cap, double db1,
-                       double db2, T eps, long long* __restrict__ step,
-                       unsigned* __restrict__ done, const int* __restrict__ skip,
-                       T* m1, T* v1, const int* __restrict__ cur) {
-  if (skip && *skip) return;  // uniform over the grid: nobody touches the counter
-  if (cur && *cur) {  // ping-pong moments (layer state): the current pair is (m1, v1)
-    m = m1;
-    v = v1;
-  }
+//
+// kChecked (layer state with ping-pong moments): the finiteness check of the
+// gradient is fused in -- every block reads the current moment pair, writes
+// the other one, and latches the flag on a non-finite gradient element; the
+// last block flips the pair and advances the step only when the flag is clear
+// (k_check_finite + k_adam in one pass, the same outcome).
+template <typename T, bool kChecked>
+__global__ void k_adam(long long cnt, const T* __restrict__ g, T* m, T* v, T* __restrict__ delta,
+                       T b1, T omb1, T b2, T omb2, const double2* __restrict__ table,
+                       long long cap, double db1, double db2, T eps,
+                       long long* __restrict__ step, unsigned* __restrict__ done, int* skip,
+                       T* m1, T* v1, int* __restrict__ cur) {
+  if (!kChecked && skip && *skip) return;  // uniform over the grid: nobody touches the counter
+  const int which = cur ? *cur : 0;
+  // ping-pong moments (layer state): the current pair is (m1, v1) when *cur
+  T* mi = which ? m1 : m;
+  T* vi = which ? v1 : v;
+  T* mo = kChecked ? (which ? m : m1) : mi;  // unchecked: in place
+  T* vo = kChecked ? (which ? v : v1) : vi;
   const long long t = *step + 1;
   double2 c;
   if (t <= cap) {
@@ -42,40 +49,53 @@ __global__ void k_adam(long long cnt, const T* __restrict__ g, T* __restrict__ m
     c.y = 1.0 - pow(db2, static_cast<double>(t));
   }
   const T c1 = static_cast<T>(c.x), c2 = static_cast<T>(c.y);
-  auto one = [&](T gi, T& mo, T& vo) {  // returns delta; updates the moments in place
-    return adam_elem(gi, mo, vo, b1, omb1, b2, omb2, c1, c2, eps);
+  bool bad = false;
+  auto one = [&](T gi, T& mv, T& vv) {  // returns delta; updates the moments in place
+    if constexpr (kChecked) bad |= !isfinite(gi);
+    return adam_elem(gi, mv, vv, b1, omb1, b2, omb2, c1, c2, eps);
   };
   long long i0 = 0;
   if constexpr (sizeof(T) == 4) {
     // 16-byte vector path (all of a layer's blocks are 16-byte aligned, cnt % 4 == 0)
-    if ((cnt & 3) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
-                            reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(delta)) & 15) == 0) {
+    if ((cnt & 3) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(mi) |
+                            reinterpret_cast<uintptr_t>(vi) | reinterpret_cast<uintptr_t>(mo) |
+                            reinterpret_cast<uintptr_t>(vo) | reinterpret_cast<uintptr_t>(delta)) & 15) == 0) {
       const long long n4 = cnt >> 2;
       for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
            i += (long long)gridDim.x * blockDim.x) {
         const float4 gv = reinterpret_cast<const float4*>(g)[i];
-        float4 mv = reinterpret_cast<float4*>(m)[i];
-        float4 vv = reinterpret_cast<float4*>(v)[i];
+        float4 mv = reinterpret_cast<const float4*>(mi)[i];
+        float4 vv = reinterpret_cast<const float4*>(vi)[i];
         float4 dv;
         dv.x = one(gv.x, mv.x, vv.x);
         dv.y = one(gv.y, mv.y, vv.y);
         dv.z = one(gv.z, mv.z, vv.z);
         dv.w = one(gv.w, mv.w, vv.w);
-        reinterpret_cast<float4*>(m)[i] = mv;
-        reinterpret_cast<float4*>(v)[i] = vv;
+        reinterpret_cast<float4*>(mo)[i] = mv;
+        reinterpret_cast<float4*>(vo)[i] = vv;
         reinterpret_cast<float4*>(delta)[i] = dv;
       }
       i0 = cnt;
     }
   }
   for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
-       i += (long long)gridDim.x * blockDim.x)
-    delta[i] = one(g[i], m[i], v[i]);
+       i += (long long)gridDim.x * blockDim.x) {
+    T mv = mi[i], vv = vi[i];
+    delta[i] = one(g[i], mv, vv);
+    mo[i] = mv;
+    vo[i] = vv;
+  }
+  if constexpr (kChecked) {
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(skip, 1);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    __threadfence();  // (checked: this block's latch and moments before its done count)
     if (atomicAdd(done, 1u) == gridDim.x - 1) {  // every block has read *step
-      *step = t;
+      if (!kChecked || atomicOr(skip, 0) == 0) {
+        if (kChecked) *cur = 1 - which;
+        *step = t;
+      }
       *done = 0u;
       __threadfence();
     }
@@ -174,18 +194,22 @@ const double2* correction_table(double b1, double b2, long long* cap) {
   return cache.back()->buf.as<double2>();
 }
 
-void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st) {
+void launch_adam(Adam& a, const void* grad, void* delta, const int* skip_flag, cudaStream_t st,
+                 bool checked) {
   long long cap = 0;
   const double2* table = correction_table(a.beta1, a.beta2, &cap);
   const long long cnt = static_cast<long long>(a.count());
+  int* flag = const_cast<int*>(skip_flag);
+  if (checked) require(flag && a.cur.p, "adam: the checked update needs a flag and ping-pong moments");
   LSP_DISPATCH_ACC(a.compute, T, {
-    k_adam<T><<<grid_for(cnt), 256, 0, st>>>(
+    auto kern = checked ? k_adam<T, true> : k_adam<T, false>;
+    kern<<<grid_for(cnt), 256, 0, st>>>(
         cnt, static_cast<const T*>(grad), a.m.as<T>(), a.v.as<T>(), static_cast<T*>(delta),
         (T)a.beta1, (T)(1.0 - a.beta1), (T)a.beta2, (T)(1.0 - a.beta2), table, cap, a.beta1,
-        a.beta2, (T)a.eps, a.dstep.as<long long>(), a.done.as<unsigned>(), skip_flag,
-        a.m2.as<T>(), a.v2.as<T>(), a.cur.as<const int>());
+        a.beta2, (T)a.eps, a.dstep.as<long long>(), a.done.as<unsigned>(), flag,
+        a.m2.as<T>(), a.v2.as<T>(), a.cur.as<int>());
   })
-  after_launch("adam");
+  after_launch(checked ? "adam_checked" : "adam");
 }
 
 void launch_check_finite(size_t cnt, const void* x, lsp_dtype dt, int* flag, cudaStream_t st) {

@@ -5,6 +5,7 @@
 // for all linear layers of a block at once.  The S^T, delta^T and moment
 // buffers of the layer are contiguous, so a data-parallel caller all-reduces
 // the whole layer with one collective.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -81,6 +82,11 @@ void layer_compress(lsp_layer_s& L, cudaStream_t st) {
 
 void layer_adam(lsp_layer_s& L, bool check, cudaStream_t st) {
   int* flag = L.adam.flag.as<int>();
+  const char* e = std::getenv("LSP_FUSE_ADAM");
+  if (check && !(e && e[0] == '0')) {  // the check fused into Adam (ping-pong moments)
+    launch_adam(L.adam, L.s_t.p, L.d_t.p, flag, st, true);
+    return;
+  }
   if (check) launch_check_finite(L.count * L.dd(), L.s_t.p, L.compute, flag, st);
   launch_adam(L.adam, L.s_t.p, L.d_t.p, flag, st);
 }

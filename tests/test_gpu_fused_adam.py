@@ -77,6 +77,61 @@ def test_fused_adam_bitwise_unfused(cuda, d, split):
     assert la.adam_get(0)[2] == 4
 
 
+@pytest.mark.parametrize("d", [1536, 2048])
+def test_fused_adam_wide_d(cuda, d):
+    """d > 1024: each thread walks several 1024-column segments of its S^T row
+    (the moment staging buffer is reused per segment); 1536 leaves the last
+    segment half empty."""
+    pairs = _pairs(d=d, shapes=[(512, 640), (640, 512)])
+    la, lb, gs, wa, wb = _layers(pairs, seed=4)
+    for it in range(3):
+        la.compress_adam()
+        la.apply(1e-3)
+        lb.compress()
+        lb.adam()
+        lb.apply(1e-3)
+        for g in gs:
+            g.mul_(0.5).add_(-0.25)
+    torch.cuda.synchronize()
+    assert torch.equal(la.s_buffer(), lb.s_buffer())
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+    _same_state(la, lb, len(pairs))
+
+
+@pytest.mark.parametrize("compute,d", [("f64", 64), ("f32", 30)])
+def test_compress_adam_fallback(cuda, compute, d):
+    """Groups the fused kernel does not cover (fp64; d % 4 != 0) run stage 2 and
+    k_adam behind lsp_layer_compress_adam: the same results as the explicit pair."""
+    tdt = torch.float64 if compute == "f64" else torch.float32
+    pairs = []
+    for i, (m, n) in enumerate([(256, 320), (320, 256)]):
+        P = lsp.DeviceProjector.random(m, d, 4, lsp.derive_seed(9, KINIT, 2 * i), compute)
+        Q = lsp.DeviceProjector.random(n, d, 4, lsp.derive_seed(9, KINIT, 2 * i + 1), compute)
+        pairs.append(lsp.DevicePair(P, Q))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    gs = [torch.randn(p.m, p.n, device="cuda", generator=g, dtype=tdt) for p in pairs]
+    w0 = [0.02 * torch.randn(p.m, p.n, device="cuda", generator=g, dtype=tdt) for p in pairs]
+    wa = [w.clone() for w in w0]
+    wb = [w.clone() for w in w0]
+    la, lb = lsp.Layer(pairs), lsp.Layer(pairs)
+    for i in range(len(pairs)):
+        la.bind(i, gs[i], wa[i])
+        lb.bind(i, gs[i], wb[i])
+    for _ in range(3):
+        la.compress_adam()
+        la.apply(1e-3)
+        lb.compress()
+        lb.adam()
+        lb.apply(1e-3)
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+    _same_state(la, lb, len(pairs))
+    assert la.adam_get(0)[2] == 3
+
+
 def test_fused_adam_nonfinite_keeps_state(cuda):
     """A non-finite S latches the flag, W is untouched and the ping-pong pair is
     not flipped: moments and step stay those of the last finite step (k_adam's
@@ -184,3 +239,38 @@ def test_schedules_fuse_bitwise_unfused(cuda, mode):
         y.check()
         _same_state(x, y, len(x.pairs))
         assert y.adam_get(0)[2] == steps
+
+
+def test_checked_adam_bitwise(cuda):
+    """Data-parallel form: Adam with the finiteness re-check fused in
+    (lsp_layer_adam(check_finite=1) after an all-reduce: one ping-pong kernel
+    instead of k_check_finite + k_adam) equals the unchecked update on finite
+    S, and on a non-finite S latches the flag and leaves W, moments and step."""
+    pairs = _pairs()
+    la, lb, gs, wa, wb = _layers(pairs, seed=6)
+    for it in range(3):
+        la.compress()
+        la.adam(check_finite=True)
+        la.apply(1e-3)
+        lb.compress()
+        lb.adam()
+        lb.apply(1e-3)
+        for g in gs:
+            g.mul_(0.9).add_(0.05)
+    torch.cuda.synchronize()
+    for x, y in zip(wa, wb):
+        assert torch.equal(x, y)
+    _same_state(la, lb, len(pairs))
+    la.s_buffer()[1, 3, 2] = float("nan")  # e.g. a rank contributed a non-finite S
+    w_before = [w.clone() for w in wa]
+    la.adam(check_finite=True)
+    la.apply(1e-3)
+    with pytest.raises(lsp.NumericError):
+        la.check()
+    for x, y in zip(wa, w_before):
+        assert torch.equal(x, y)
+    _same_state(la, lb, len(pairs))
+    la.update(1e-3, check_finite=True)  # the S buffer still holds the NaN
+    with pytest.raises(lsp.NumericError):
+        la.check()
+    assert la.adam_get(0)[2] == 3
