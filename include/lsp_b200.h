@@ -269,7 +269,9 @@ int lsp_layer_compress_finish_adam(lsp_layer_t layer, lsp_stream_t stream);
  * all-reduce) and W_i -= lr * P_i delta_i Q_i^T; skipped if the flag is set. */
 int lsp_layer_update(lsp_layer_t layer, double lr, int check_finite, lsp_stream_t stream);
 /* The two halves of lsp_layer_update: Adam -> delta^T, then the fused
- * decompress-and-apply of every matrix (one grouped launch each). */
+ * decompress-and-apply of every matrix (one grouped launch each).  With
+ * check_finite the re-check runs inside the Adam launch (the moments'
+ * ping-pong pair is flipped only when every S element was finite). */
 int lsp_layer_adam(lsp_layer_t layer, int check_finite, lsp_stream_t stream);
 int lsp_layer_apply(lsp_layer_t layer, double lr, lsp_stream_t stream);
 /* compress + update. */
