@@ -336,8 +336,8 @@ int lsp_layer_apply_finish(lsp_layer_t L, double lr, lsp_stream_t stream) {
 int lsp_layer_step(lsp_layer_t L, double lr, lsp_stream_t stream) {
   return guard_layer([&] {
     require(L != nullptr, "layer_step: null layer");
-    layer_compress(*L, as_stream(stream));
-    layer_update(*L, lr, false, as_stream(stream));
+    layer_compress_adam(*L, as_stream(stream));  // one rank: Adam in the stage-2 epilogue
+    layer_apply(*L, lr, as_stream(stream));
   });
 }
 
