@@ -572,7 +572,7 @@ constexpr int kS2V = 2;  // float4 column chunks per thread (d = 1024: the whole
 // plain epilogue load made the fused kernel slower than the pair), and more
 // S^T rows per CTA (fewer done-counter atomics) measured slower (2: +0.3 ms,
 // 4: +1.0 ms per C4 step).
-constexpr int kS2AdamMinBlocks = 8;  // CTAs per SM the fused kernel is register-bounded for
+constexpr int kS2AdamMinBlocks = 8;  // 128-thread CTAs per SM the fused kernel is register-bounded for
 struct S2Adam {
   long long off[kMaxGroup];  // element offset of A.mat[i]'s block in the layer state
   float *m0, *v0, *m1, *v1, *delta;
@@ -644,14 +644,15 @@ __global__ void __launch_bounds__(kS2Threads) k_stage2_f4(const __grid_constant_
   if (A.flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(A.flag, 1);
 }
 
-__global__ void __launch_bounds__(kS2Threads, kS2AdamMinBlocks)
+template <int NT>
+__global__ void __launch_bounds__(NT, kS2AdamMinBlocks * 128 / NT)
     k_stage2_adam_f4(const __grid_constant__ S2Args A, const __grid_constant__ S2Adam K) {
   const S2Mat& M = A.mat[blockIdx.y];
   const int b = blockIdx.x, d = A.d;
   const int e0 = __ldg(M.ptr + b), e1 = __ldg(M.ptr + b + 1);
   bool bad = false;
   // the CTA's current moments, staged by cp.async while the gathers run
-  __shared__ __align__(16) float4 mv_s[2 * kS2V * kS2Threads];
+  __shared__ __align__(16) float4 mv_s[2 * kS2V * NT];
   // read before this CTA counts itself done: the last CTA's flip comes after
   const long long t = *K.step + 1;
   const int which = *K.cur;
@@ -663,17 +664,17 @@ __global__ void __launch_bounds__(kS2Threads, kS2AdamMinBlocks)
     c.y = 1.0 - pow(K.db2, static_cast<double>(t));
   }
   const float c1 = static_cast<float>(c.x), c2 = static_cast<float>(c.y);
-  for (int a_base = 4 * threadIdx.x; a_base < d; a_base += 4 * kS2Threads * kS2V) {
+  for (int a_base = 4 * threadIdx.x; a_base < d; a_base += 4 * NT * kS2V) {
     {
       const long long i0 = K.off[blockIdx.y] + static_cast<long long>(b) * d + a_base;
       const float* mi = which ? K.m1 : K.m0;
       const float* vi = which ? K.v1 : K.v0;
 #pragma unroll
       for (int c = 0; c < kS2V; ++c) {
-        const bool in = a_base + c * 4 * kS2Threads < d;
-        const long long i = i0 + c * 4 * kS2Threads;
-        cp_async16(&mv_s[(2 * c) * kS2Threads + threadIdx.x], in ? mi + i : mi, in ? 16 : 0);
-        cp_async16(&mv_s[(2 * c + 1) * kS2Threads + threadIdx.x], in ? vi + i : vi, in ? 16 : 0);
+        const bool in = a_base + c * 4 * NT < d;
+        const long long i = i0 + c * 4 * NT;
+        cp_async16(&mv_s[(2 * c) * NT + threadIdx.x], in ? mi + i : mi, in ? 16 : 0);
+        cp_async16(&mv_s[(2 * c + 1) * NT + threadIdx.x], in ? vi + i : vi, in ? 16 : 0);
       }
       asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -682,7 +683,7 @@ __global__ void __launch_bounds__(kS2Threads, kS2AdamMinBlocks)
 #pragma unroll
     for (int c = 0; c < kS2V; ++c) {
       acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      ok[c] = a_base + c * 4 * kS2Threads < d;
+      ok[c] = a_base + c * 4 * NT < d;
     }
     int e = e0;
     for (; e + 4 <= e1; e += 4) {
@@ -694,7 +695,7 @@ __global__ void __launch_bounds__(kS2Threads, kS2AdamMinBlocks)
         const float* zr = M.zt + static_cast<long long>(__ldg(M.row + e + u)) * M.ldz + a_base;
 #pragma unroll
         for (int c = 0; c < kS2V; ++c)
-          z[u][c] = ok[c] ? __ldg(reinterpret_cast<const float4*>(zr + c * 4 * kS2Threads))
+          z[u][c] = ok[c] ? __ldg(reinterpret_cast<const float4*>(zr + c * 4 * NT))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(kS2Threads, kS2AdamMinBlocks)
 #pragma unroll
       for (int c = 0; c < kS2V; ++c) {
         if (!ok[c]) continue;
-        const float4 z = __ldg(reinterpret_cast<const float4*>(zr + c * 4 * kS2Threads));
+        const float4 z = __ldg(reinterpret_cast<const float4*>(zr + c * 4 * NT));
         acc[c].x = fmaf(q, z.x, acc[c].x);
         acc[c].y = fmaf(q, z.y, acc[c].y);
         acc[c].z = fmaf(q, z.z, acc[c].z);
@@ -724,13 +725,13 @@ __global__ void __launch_bounds__(kS2Threads, kS2AdamMinBlocks)
     for (int c = 0; c < kS2V; ++c) {
       if (!ok[c]) continue;
       bad |= !(isfinite(acc[c].x) && isfinite(acc[c].y) && isfinite(acc[c].z) && isfinite(acc[c].w));
-      const long long el = static_cast<long long>(b) * d + a_base + c * 4 * kS2Threads;
+      const long long el = static_cast<long long>(b) * d + a_base + c * 4 * NT;
       *reinterpret_cast<float4*>(M.s_t + el) = acc[c];
       {
         const long long i = K.off[blockIdx.y] + el;
         asm volatile("cp.async.wait_all;\n" ::: "memory");  // own copies only
-        float4 mv = mv_s[(2 * c) * kS2Threads + threadIdx.x];
-        float4 vv = mv_s[(2 * c + 1) * kS2Threads + threadIdx.x];
+        float4 mv = mv_s[(2 * c) * NT + threadIdx.x];
+        float4 vv = mv_s[(2 * c + 1) * NT + threadIdx.x];
         float4 dv;
         dv.x = adam_elem(acc[c].x, mv.x, vv.x, K.b1, K.omb1, K.b2, K.omb2, c1, c2, K.eps);
         dv.y = adam_elem(acc[c].y, mv.y, vv.y, K.b1, K.omb1, K.b2, K.omb2, c1, c2, K.eps);
@@ -938,7 +939,17 @@ bool launch_stage2_adam_group(const std::vector<S1Job>& jobs, const void* s_base
   K.eps = static_cast<float>(a.eps);
   K.step = a.dstep.as<long long>();
   K.done = a.done.as<unsigned>();
-  k_stage2_adam_f4<<<dim3(d, A.count), kS2Threads, 0, st>>>(A, K);
+  // threads per S^T row: 8 columns each, whole warps, at most kS2Threads (narrow
+  // d: no idle warps, more CTAs per SM; C2 d = 512: 64 threads)
+  const int nt = std::min(kS2Threads, std::max(32, static_cast<int>(round_up(ceil_div(d, 8), 32))));
+  if (nt == 32)
+    k_stage2_adam_f4<32><<<dim3(d, A.count), 32, 0, st>>>(A, K);
+  else if (nt == 64)
+    k_stage2_adam_f4<64><<<dim3(d, A.count), 64, 0, st>>>(A, K);
+  else if (nt == 96)
+    k_stage2_adam_f4<96><<<dim3(d, A.count), 96, 0, st>>>(A, K);
+  else
+    k_stage2_adam_f4<kS2Threads><<<dim3(d, A.count), kS2Threads, 0, st>>>(A, K);
   after_launch("stage2_adam");
   return true;
 }
