@@ -134,3 +134,12 @@ def test_schedule_set_pipeline_rejects_bad_args():
 def test_schedule_set_partition_rejects_bad_args():
     with pytest.raises(lsp.InvalidArgument):
         lsp.lib.schedule_set_partition(None, 64, None, None)
+
+
+def test_layer_fused_entries_reject_null_layer():
+    """lsp_layer_compress_adam / _compress_finish_adam (stage 2 with Adam fused)
+    check their handle before touching the device."""
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.layer_compress_adam(None, None)
+    with pytest.raises(lsp.InvalidArgument):
+        lsp.lib.layer_compress_finish_adam(None, None)
